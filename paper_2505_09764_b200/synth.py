@@ -1,0 +1,225 @@
+"""GPU schedule synthesis behind tiersched's scheduler API.
+
+Drop-in entry points (same names, arguments and error classes as the
+reference):
+
+    synthesize_fast(d, t) -> Schedule                 pipeline.py:52
+    build_balance_plan(d, t) -> BalancePlan           balance.py:139
+    decompose_server_matrix(s) -> Decomposition       birkhoff.py:269
+    embed_doubly_stochastic(s) -> (embedded, aux)     birkhoff.py:75
+    decompose(embedded) -> list[PermutationStage]     birkhoff.py:140
+
+plus the batched device API used by the executor and the benchmarks:
+
+    synthesize_packed(D, n, m) -> SynthBuffers  (D: cuda int64 [B,G,G])
+
+Every call runs the sm_100a kernels in libfastb200.so on the current CUDA
+stream.  There is no CPU fallback: without a CUDA device these raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .model import (DemandMatrix, InternalInvariantError, ServerMatrix, Topology,
+                    ValidationError)
+from .schedule import (MOVE_DTYPE, BalancePlan, Decomposition, PackedSchedule,
+                       PermutationStage, Schedule)
+
+
+def stage_cap(n: int) -> int:
+    return n * n - 2 * n + 2
+
+
+def _device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2505_09764_b200 synthesis needs a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _stream_handle(stream: torch.cuda.Stream | None) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class SynthBuffers:
+    """Device-resident packed schedules for a batch (fast_sched_bufs)."""
+
+    def __init__(self, B: int, n: int, m: int, device: torch.device | None = None,
+                 with_balance: bool = True):
+        dev = device or _device()
+        G, T, S, K = n * m, n * (n - 1), max(m - 1, 1), stage_cap(n)
+        self.B, self.n, self.m = B, n, m
+        i64, i32, u8 = torch.int64, torch.int32, torch.uint8
+        e = lambda *shape, dt: torch.empty(shape, dtype=dt, device=dev)  # noqa: E731
+        gb = G if with_balance else 1
+        self.balanced = e(B, gb, gb, dt=i64)
+        self.server = e(B, n, n, dt=i64)
+        self.move_count = e(B, T, dt=i32)
+        self.moves = e(B, T, S, 2, dt=i64)  # fast_move is 16 bytes
+        self.common_sum = e(B, dt=i64)
+        self.aux = e(B, n, n, dt=i64)
+        self.n_raw = e(B, dt=i32)
+        self.stage_weight = e(B, K, dt=i64)
+        self.stage_perm = e(B, K, n, dt=u8)
+        self.stage_bytes = e(B, K, n, dt=i64)
+        self.n_stages = e(B, dt=i32)
+        self.stage_order = e(B, K, dt=i32)
+        self.status = e(B, dt=i32)
+        ws = _lib.load().fast_synth_workspace_bytes(B, n)
+        self.workspace = e(max(int(ws), 16), dt=u8)
+        self._struct = _lib.FastSchedBufs(*(t.data_ptr() for t in (
+            self.balanced, self.server, self.move_count, self.moves, self.common_sum,
+            self.aux, self.n_raw, self.stage_weight, self.stage_perm, self.stage_bytes,
+            self.n_stages, self.stage_order, self.status, self.workspace)))
+
+    @property
+    def struct(self) -> _lib.FastSchedBufs:
+        return self._struct
+
+    def output_nbytes(self) -> int:
+        """Bytes of the packed schedule (what a D2H of the result moves)."""
+        ts = (self.balanced, self.server, self.move_count, self.moves, self.common_sum,
+              self.aux, self.n_raw, self.stage_weight, self.stage_perm, self.stage_bytes,
+              self.n_stages, self.stage_order, self.status)
+        return sum(t.numel() * t.element_size() for t in ts)
+
+    def host(self, b: int | None = None) -> list[PackedSchedule]:
+        """Copy to host and split per matrix (synchronizes)."""
+        h = {k: getattr(self, k).cpu().numpy() for k in (
+            "balanced", "server", "move_count", "moves", "common_sum", "aux", "n_raw",
+            "stage_weight", "stage_perm", "stage_bytes", "n_stages", "stage_order", "status")}
+        moves = h["moves"].view(MOVE_DTYPE).reshape(h["moves"].shape[:3])
+        idx = range(self.B) if b is None else [b]
+        out = []
+        for i in idx:
+            k, s = int(h["n_raw"][i]), int(h["n_stages"][i])
+            out.append(PackedSchedule(
+                n=self.n, m=self.m, status=int(h["status"][i]), balanced=h["balanced"][i],
+                server=h["server"][i], move_count=h["move_count"][i], moves=moves[i],
+                common_sum=int(h["common_sum"][i]), aux=h["aux"][i], n_raw=k,
+                stage_weight=h["stage_weight"][i][:k], stage_perm=h["stage_perm"][i][:k],
+                stage_bytes=h["stage_bytes"][i][:k], n_stages=s,
+                stage_order=h["stage_order"][i][:s]))
+        return out
+
+
+def synthesize_packed(D: torch.Tensor, n: int, m: int, bufs: SynthBuffers | None = None,
+                      stream: torch.cuda.Stream | None = None) -> SynthBuffers:
+    """Batched synthesize_fast on the device (stream-ordered, no sync).
+
+    D: cuda int64 [B, n*m, n*m].  Per-matrix status lands in bufs.status.
+    """
+    if D.dtype != torch.int64 or not D.is_cuda or D.dim() != 3:
+        raise ValidationError("D must be a cuda int64 tensor [B, G, G]")
+    B = D.shape[0]
+    if D.shape[1:] != (n * m, n * m):
+        raise ValidationError(f"D shape {tuple(D.shape)} does not match n={n}, m={m}")
+    D = D.contiguous()
+    if bufs is None:
+        bufs = SynthBuffers(B, n, m, D.device)
+    rc = _lib.load().fast_synth_batch(ctypes.c_void_p(D.data_ptr()), B, n, m,
+                                      ctypes.byref(bufs.struct), _stream_handle(stream))
+    _lib.check_rc(rc, "fast_synth_batch")
+    return bufs
+
+
+def _raise_status(code: int, what: str) -> None:
+    if code == _lib.FAST_EVALIDATION:
+        raise ValidationError(f"{what}: invalid input")
+    if code != _lib.FAST_OK:
+        raise InternalInvariantError(f"{what}: internal invariant broken (status {code})")
+
+
+def _demand_batch(ds: Sequence[DemandMatrix] | np.ndarray, t: Topology) -> np.ndarray:
+    if isinstance(ds, np.ndarray):
+        return np.ascontiguousarray(ds, dtype=np.int64)
+    for d in ds:
+        if (d.n_servers, d.gpus_per_server) != (t.n_servers, t.gpus_per_server):
+            raise ValidationError(
+                f"matrix is {d.n_servers}x{d.gpus_per_server} but topology is "
+                f"{t.n_servers}x{t.gpus_per_server}")
+    return np.stack([d.sizes for d in ds]).astype(np.int64, copy=False)
+
+
+def synthesize_fast_batch(ds: Sequence[DemandMatrix] | np.ndarray, t: Topology) -> list[Schedule]:
+    """synthesize_fast over many matrices in one set of kernel launches."""
+    n, m = t.n_servers, t.gpus_per_server
+    D = torch.from_numpy(_demand_batch(ds, t)).to(_device())
+    packed = synthesize_packed(D, n, m).host()
+    out = []
+    for p in packed:
+        _raise_status(p.status, "synthesize_fast")
+        out.append(p.to_schedule())
+    return out
+
+
+def synthesize_fast(d: DemandMatrix, t: Topology) -> Schedule:
+    """Balance, reduce, decompose, strip, sort -- on the GPU (pipeline.py:52)."""
+    return synthesize_fast_batch([d], t)[0]
+
+
+def build_balance_plan(d: DemandMatrix, t: Topology) -> BalancePlan:
+    """Phase 1 only (balance.py:139-174), on the GPU."""
+    n, m = t.n_servers, t.gpus_per_server
+    D = torch.from_numpy(_demand_batch([d], t)).to(_device())
+    bufs = SynthBuffers(1, n, m, D.device)
+    rc = _lib.load().fast_balance_batch(ctypes.c_void_p(D.data_ptr()), 1, n, m,
+                                        ctypes.byref(bufs.struct), _stream_handle(None))
+    _lib.check_rc(rc, "fast_balance_batch")
+    st = int(bufs.status.cpu()[0])
+    _raise_status(st, "build_balance_plan")
+    h = {k: getattr(bufs, k)[0].cpu().numpy() for k in ("balanced", "server", "move_count", "moves")}
+    p = PackedSchedule(n=n, m=m, status=st, balanced=h["balanced"], server=h["server"],
+                       move_count=h["move_count"],
+                       moves=h["moves"].view(MOVE_DTYPE).reshape(h["moves"].shape[:2]),
+                       common_sum=0, aux=np.zeros((n, n), np.int64), n_raw=0,
+                       stage_weight=np.zeros(0, np.int64), stage_perm=np.zeros((0, n), np.uint8),
+                       stage_bytes=np.zeros((0, n), np.int64), n_stages=0,
+                       stage_order=np.zeros(0, np.int32))
+    return p.balance_plan()
+
+
+def _decompose_packed(S: np.ndarray, mode: int) -> PackedSchedule:
+    S = np.ascontiguousarray(S, dtype=np.int64)
+    n = S.shape[0]
+    if S.ndim != 2 or S.shape[1] != n:
+        raise ValidationError("decompose expects a square matrix")
+    dev = _device()
+    St = torch.from_numpy(S[None].copy()).to(dev)
+    bufs = SynthBuffers(1, n, 1, dev, with_balance=False)
+    rc = _lib.load().fast_decompose_batch(ctypes.c_void_p(St.data_ptr()), 1, n, mode,
+                                          ctypes.byref(bufs.struct), _stream_handle(None))
+    _lib.check_rc(rc, "fast_decompose_batch")
+    return bufs.host(0)[0]
+
+
+def decompose_server_matrix(s: ServerMatrix) -> Decomposition:
+    """Embed + decompose a server matrix (birkhoff.py:269-280), on the GPU."""
+    p = _decompose_packed(s.totals, _lib.FAST_DEC_SERVER)
+    _raise_status(p.status, "decompose_server_matrix")
+    return p.decomposition()
+
+
+def embed_doubly_stochastic(s: ServerMatrix) -> tuple[np.ndarray, np.ndarray]:
+    """Northwest-corner embedding (birkhoff.py:75-108), on the GPU."""
+    p = _decompose_packed(s.totals, _lib.FAST_DEC_SERVER)
+    _raise_status(p.status, "embed_doubly_stochastic")
+    return s.off_diagonal() + p.aux, p.aux.copy()
+
+
+def decompose(embedded: np.ndarray) -> list[PermutationStage]:
+    """Birkhoff peeling of a doubly stochastic matrix (birkhoff.py:140-222)."""
+    e = np.asarray(embedded)
+    if e.ndim != 2 or e.shape[0] != e.shape[1]:
+        raise ValidationError("decompose expects a square matrix")
+    if not np.issubdtype(e.dtype, np.integer):
+        raise ValidationError("decompose expects an integer matrix")
+    p = _decompose_packed(e.astype(np.int64), _lib.FAST_DEC_DOUBLY_STOCHASTIC)
+    _raise_status(p.status, "decompose")
+    return list(p.raw_stages())
