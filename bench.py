@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""Benchmark of the FAST All-to-All(v) hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N = 1 (default): BASELINE config 5, schedule-synthesis scaling -- one step is
+synthesize_fast over a batch of 1000 Zipf(0.8) traffic matrices of
+n = 128 virtual servers x 8 GPUs (the largest single-GPU configuration),
+inputs resident in HBM.  N > 1 (torchrun, one rank per GPU): the alltoallv
+workload (BASELINE config 2 shape) executed by the P2P stage executor over
+NVSwitch (see bench_alltoallv in this file).
+
+Rank 0 prints ONE JSON line.  ``--impl reference`` times the reference's own
+CPU implementation (tiersched from baseline/_ref, else the C oracle port) on
+the same config and prints the same line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+HBM_FALLBACK_GBS = 6650.0
+
+
+def measured_peaks() -> tuple[dict, str]:
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh), "measured"
+    return {"hbm_gbs": HBM_FALLBACK_GBS}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self) -> dict:
+        rows = []
+        if self.path and os.path.exists(self.path):
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9 and parts[1].isdigit():
+                    rows.append(parts)
+            os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [int(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": int(statistics.median(busy)), "sm_max_mhz": int(rows[0][2]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# config 5: batched schedule synthesis on 1 GPU
+
+def synth_inputs(args, device):
+    from paper_2505_09764_b200 import workloads
+
+    G = args.n * args.m
+    return workloads.zipf_batch_device(range(args.batch), G, args.skew, args.total, device)
+
+
+def algorithmic_bytes_decompose(n: int, n_raw) -> int:
+    # read server matrix, write aux, write each raw stage (weight + perm + bytes)
+    return int(sum(16 * n * n + int(k) * (8 + 9 * n) for k in n_raw))
+
+
+def bench_synth(args) -> dict:
+    import torch
+
+    from paper_2505_09764_b200 import _lib, synth
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    lib = _lib.load()
+    n, m, B = args.n, args.m, args.batch
+    G = n * m
+    D = synth_inputs(args, dev)
+    bufs = synth.SynthBuffers(B, n, m, dev)
+    stream = torch.cuda.current_stream()
+    sh = ctypes.c_void_p(stream.cuda_stream)
+
+    def make_events(k):
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(k)]
+        for row in evs:
+            for e in row:
+                e.record(stream)  # materialise the handles
+        return evs
+
+    def step(ev_row=None):
+        arr = None
+        if ev_row is not None:
+            arr = (ctypes.c_void_p * 4)(*[e.cuda_event for e in ev_row])
+        rc = lib.fast_synth_batch_ev(ctypes.c_void_p(D.data_ptr()), B, n, m,
+                                     ctypes.byref(bufs.struct), sh, arr)
+        _lib.check_rc(rc, "fast_synth_batch_ev")
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    status = bufs.status.cpu()
+    if int(status.abs().max()) != 0:
+        raise RuntimeError(f"synthesis failed on {int((status != 0).sum())} matrices")
+
+    evs = make_events(args.steps)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    with ClockSampler(0) as clk:
+        t0.record(stream)
+        for k in range(args.steps):
+            step(evs[k])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    total_ms = t0.elapsed_time(t1)
+    per = {"balance_kernel": 0.0, "decompose_kernel": 0.0, "sort_kernel": 0.0}
+    for row in evs:
+        per["balance_kernel"] += row[0].elapsed_time(row[1])
+        per["decompose_kernel"] += row[1].elapsed_time(row[2])
+        per["sort_kernel"] += row[2].elapsed_time(row[3])
+    per = {k: v / args.steps for k, v in per.items()}
+    ms_step = total_ms / args.steps
+    n_raw = bufs.n_raw.cpu().tolist()
+
+    peaks, peak_kind = measured_peaks()
+    hbm = float(peaks["hbm_gbs"])
+    alg = {"balance_kernel": 16 * G * G * B,
+           "decompose_kernel": algorithmic_bytes_decompose(n, n_raw),
+           "sort_kernel": int(sum(12 * 2 * k for k in n_raw))}
+    dom = max(per, key=per.get)
+    achieved = alg[dom] / (per[dom] * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        key = f"{dom}/n{n}_m{m}_B{B}"
+        traffic = json.load(open(tf)).get(key)
+    roofline = {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 5), "traffic": traffic, "kernel": dom,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                "kernel_ms": {k: round(v, 4) for k, v in per.items()},
+                "balance_kernel_gbs": round(alg["balance_kernel"] / (per["balance_kernel"] * 1e-3) / 1e9, 1),
+                "balance_kernel_frac": round(alg["balance_kernel"] / (per["balance_kernel"] * 1e-3) / 1e9 / hbm, 4),
+                "note": "decompose is a dependent chain of <= n^2-2n+2 peels per matrix "
+                        "(latency-bound); balance is the HBM-bound kernel"}
+
+    # ---- e2e: host (pinned) D -> device -> synth -> packed schedule -> host
+    e2e = None
+    if not args.no_e2e:
+        Dh = torch.empty(D.shape, dtype=D.dtype, pin_memory=True)
+        Dh.copy_(D)
+        outs = [getattr(bufs, k) for k in ("balanced", "server", "move_count", "moves",
+                                           "common_sum", "aux", "n_raw", "stage_weight",
+                                           "stage_perm", "stage_bytes", "n_stages",
+                                           "stage_order", "status")]
+        hosts = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in outs]
+        Dd = torch.empty_like(D)
+        h2d = Dh.numel() * 8
+        d2h = sum(h.numel() * h.element_size() for h in hosts)
+
+        def e2e_step():
+            Dd.copy_(Dh, non_blocking=True)
+            rc = lib.fast_synth_batch(ctypes.c_void_p(Dd.data_ptr()), B, n, m,
+                                      ctypes.byref(bufs.struct), sh)
+            _lib.check_rc(rc, "fast_synth_batch")
+            for h, o in zip(hosts, outs):
+                h.copy_(o, non_blocking=True)
+
+        for _ in range(min(args.warmup, 1) or 1):
+            e2e_step()
+        torch.cuda.synchronize()
+        steps = max(1, min(args.steps, 3))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / steps
+        e2e = {"value": round(B / (ems * 1e-3), 3), "unit": "matrices/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": round(ems, 3), "steps": steps,
+               "path": "C-ABI fast_synth_batch with pinned host buffers"}
+        del Dh, hosts, Dd
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_baseline_synth(args, D)
+
+    return {
+        "metric": "schedule synthesis throughput (FAST synthesize_fast, batch of 1000 traffic "
+                  "matrices, config 5)",
+        "value": round(B / (ms_step * 1e-3), 3), "unit": "matrices/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4), "us_per_matrix": round(ms_step * 1e3 / B, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (Zipf 0.8 traffic matrices, seeds 0..B-1, generated on device)",
+        "config": {"workload": "config5_synthesis", "n_servers": n, "gpus_per_server": m,
+                   "batch": B, "zipf_skew": args.skew, "total_bytes": args.total,
+                   "l2": "inputs larger than L2 (D batch = %.1f GB)" % (B * G * G * 8 / 1e9)
+                   if B * G * G * 8 > 126e6 else "inputs within L2"},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": 3 * args.steps, "clocks": clk.summary(),
+        "stages_per_matrix_mean": round(sum(n_raw) / len(n_raw), 1),
+    }
+
+
+def cpu_baseline_synth(args, D, budget_s: float = 12.0) -> dict:
+    """C oracle port (single thread) on a bounded sample of the same batch."""
+    from oracle import oracle
+
+    n, m = args.n, args.m
+    Dh = D[: min(64, D.shape[0])].cpu().numpy()
+    oracle.synthesize_batch(Dh[:1], n, m)  # load / warm
+    done, t0 = 0, time.perf_counter()
+    while done < Dh.shape[0]:
+        oracle.synthesize_batch(Dh[done:done + 1], n, m)
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    el = time.perf_counter() - t0
+    return {"value": round(done / el, 4), "unit": "matrices/s", "cores": 1, "kind": "port",
+            "sample": f"{done} matrices of the benchmark batch (n={n}, m={m}), "
+                      f"C restatement oracle/fast_oracle.c, 1 thread, {el:.1f} s"}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: tiersched (baseline/_ref) on the host cores
+
+def _ref_worker_init(path):
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, path)
+
+
+def _ref_synth_one(task):
+    import numpy as np
+    import tiersched as ts
+
+    n, m, sizes = task
+    d = ts.DemandMatrix(n_servers=n, gpus_per_server=m, sizes=np.asarray(sizes, np.int64))
+    t = ts.Topology(n, m, 900e9, 900e9)
+    t0 = time.perf_counter()
+    ts.synthesize_fast(d, t)
+    return time.perf_counter() - t0
+
+
+def reference_synth(args) -> dict:
+    import multiprocessing as mp
+
+    from paper_2505_09764_b200 import workloads
+
+    ref = os.path.join(REPO, "baseline", "_ref")
+    have_ref = os.path.isdir(os.path.join(ref, "tiersched"))
+    cores = os.cpu_count() or 1
+    n, m = args.n, args.m
+    G = n * m
+    sample = [workloads.zipf_sizes(s, G, args.skew, args.total) for s in range(cores)]
+    if have_ref:
+        pool = mp.get_context("spawn").Pool(cores, initializer=_ref_worker_init, initargs=(ref,))
+
+        def run_step():
+            t0 = time.perf_counter()
+            pool.map(_ref_synth_one, [(n, m, s) for s in sample])
+            return time.perf_counter() - t0
+        kind, what = "reference", "tiersched.synthesize_fast (baseline/_ref, unmodified Python)"
+    else:
+        from oracle import oracle
+        import numpy as np
+
+        arr = np.stack(sample)
+
+        def run_step():
+            t0 = time.perf_counter()
+            oracle.synthesize_batch(arr, n, m)
+            return time.perf_counter() - t0
+        kind, what, cores = "port", "oracle/fast_oracle.c (1 thread)", 1
+    for _ in range(args.warmup):
+        run_step()
+    times = [run_step() for _ in range(args.steps)]
+    tot = sum(times)
+    value = len(sample) * args.steps / tot
+    if have_ref:
+        pool.close()
+    return {
+        "impl": "reference",
+        "metric": "schedule synthesis throughput (FAST synthesize_fast, batch of 1000 traffic "
+                  "matrices, config 5)",
+        "value": round(value, 5), "unit": "matrices/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (Zipf 0.8 traffic matrices)",
+        "config": {"workload": "config5_synthesis", "n_servers": n, "gpus_per_server": m,
+                   "batch": args.batch, "zipf_skew": args.skew, "total_bytes": args.total},
+        "cpu_baseline": {"value": round(value, 5), "unit": "matrices/s", "cores": cores,
+                         "kind": kind,
+                         "sample": f"{len(sample)} matrices per step, one per worker process; {what}"},
+        "e2e": {"value": round(value, 5), "unit": "matrices/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+# ---------------------------------------------------------------------------
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=("auto", "synth", "alltoallv", "moe"), default="auto")
+    ap.add_argument("--n", type=int, default=128)
+    ap.add_argument("--m", type=int, default=8)
+    ap.add_argument("--batch", type=int, default=1000)
+    ap.add_argument("--skew", type=float, default=0.8)
+    ap.add_argument("--total", type=int, default=2**34)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    workload = args.workload
+    if workload == "auto":
+        workload = "synth" if args.gpus == 1 and world == 1 else "alltoallv"
+
+    if workload == "synth":
+        if rank != 0:
+            return
+        res = reference_synth(args) if args.impl == "reference" else bench_synth(args)
+        print(json.dumps(res), flush=True)
+        return
+    from bench_exec import run as run_exec
+
+    res = run_exec(args, workload)
+    if res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -81,6 +81,14 @@ size_t fast_synth_workspace_bytes(int B, int n);
 int fast_synth_batch(const int64_t *D, int B, int n, int m,
                      const fast_sched_bufs *out, void *stream);
 
+/* fast_synth_batch with timing events: if `events` is non-NULL it points to
+ * four cudaEvent_t recorded on `stream` before the balance kernel, after it,
+ * after the decompose kernel and after the sort kernel (per-kernel device
+ * time for the benchmark's roofline). */
+int fast_synth_batch_ev(const int64_t *D, int B, int n, int m,
+                        const fast_sched_bufs *out, void *stream,
+                        void *const *events);
+
 /* build_balance_plan only (balance.py:139-174): fills balanced, server,
  * move_count, moves, status. */
 int fast_balance_batch(const int64_t *D, int B, int n, int m,

@@ -47,6 +47,9 @@ SIGNATURES: list[tuple[str, object, list]] = [
     ("fast_synth_batch", ctypes.c_int,
      [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
       ctypes.POINTER(FastSchedBufs), ctypes.c_void_p]),
+    ("fast_synth_batch_ev", ctypes.c_int,
+     [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+      ctypes.POINTER(FastSchedBufs), ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
     ("fast_balance_batch", ctypes.c_int,
      [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
       ctypes.POINTER(FastSchedBufs), ctypes.c_void_p]),

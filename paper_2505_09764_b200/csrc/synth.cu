@@ -670,7 +670,8 @@ int launch_balance(const int64_t* D, int B, int n, int m,
 }
 
 int launch_decompose(const int64_t* S, int B, int n, int mode, int check_total,
-                     const fast_sched_bufs* out, cudaStream_t s) {
+                     const fast_sched_bufs* out, cudaStream_t s,
+                     cudaEvent_t after_decompose = nullptr) {
   const size_t smem = dec_smem_bytes(n) * kDecWarps;
   if (cudaFuncSetAttribute(decompose_kernel,
                            cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -680,6 +681,8 @@ int launch_decompose(const int64_t* S, int B, int n, int mode, int check_total,
   decompose_kernel<<<grid, kDecWarps * 32, smem, s>>>(S, B, n, mode,
                                                       check_total, *out);
   if (cudaGetLastError() != cudaSuccess) return FAST_ECUDA;
+  if (after_decompose && cudaEventRecord(after_decompose, s) != cudaSuccess)
+    return FAST_ECUDA;
   const size_t ssmem = sort_smem_bytes(n);
   if (cudaFuncSetAttribute(sort_kernel,
                            cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -729,16 +732,29 @@ int fast_decompose_batch(const int64_t* S, int B, int n, int mode,
   return launch_decompose(S, B, n, mode, 0, out, s);
 }
 
-int fast_synth_batch(const int64_t* D, int B, int n, int m,
-                     const fast_sched_bufs* out, void* stream) {
+int fast_synth_batch_ev(const int64_t* D, int B, int n, int m,
+                        const fast_sched_bufs* out, void* stream,
+                        void* const* events) {
   if (bad_shape(B, n, m) || !out) return FAST_EVALIDATION;
   if (B == 0) return FAST_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  cudaEvent_t const* ev = (cudaEvent_t const*)events;
+  if (ev && cudaEventRecord(ev[0], s) != cudaSuccess) return FAST_ECUDA;
   if (cudaMemsetAsync(out->status, 0, sizeof(int32_t) * B, s) != cudaSuccess)
     return FAST_ECUDA;
   int rc = launch_balance(D, B, n, m, out, s);
   if (rc != FAST_OK) return rc;
-  return launch_decompose(out->server, B, n, FAST_DEC_SERVER, 1, out, s);
+  if (ev && cudaEventRecord(ev[1], s) != cudaSuccess) return FAST_ECUDA;
+  rc = launch_decompose(out->server, B, n, FAST_DEC_SERVER, 1, out, s,
+                        ev ? ev[2] : nullptr);
+  if (rc != FAST_OK) return rc;
+  if (ev && cudaEventRecord(ev[3], s) != cudaSuccess) return FAST_ECUDA;
+  return FAST_OK;
+}
+
+int fast_synth_batch(const int64_t* D, int B, int n, int m,
+                     const fast_sched_bufs* out, void* stream) {
+  return fast_synth_batch_ev(D, B, n, m, out, stream, nullptr);
 }
 
 }  // extern "C"

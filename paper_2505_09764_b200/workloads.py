@@ -74,6 +74,56 @@ def zipf_sizes(seed: int, g: int, skew: float, total_bytes: int) -> np.ndarray:
     return sizes
 
 
+def _zipf_base(pairs: int, skew: float, total_bytes: int) -> np.ndarray:
+    """Rank-ordered integer shares; independent of the seed."""
+    ranks = np.arange(1, pairs + 1, dtype=np.float64)
+    weights = 1.0 / ranks ** skew
+    shares = total_bytes * weights / weights.sum()
+    base = np.floor(shares).astype(np.int64)
+    leftover = total_bytes - int(base.sum())
+    if leftover > 0:
+        frac = shares - base
+        base[np.lexsort((np.arange(pairs), -frac))[:leftover]] += 1
+    return base
+
+
+def _s64(x: int) -> int:
+    return x - (1 << 64) if x >= 1 << 63 else x
+
+
+def stream_device(seeds, count: int, device):
+    """SplitMix64 outputs 0..count-1 for each seed, as int64 bit patterns
+    (torch int64 arithmetic wraps like uint64; shifts are made logical)."""
+    import torch
+
+    s = torch.as_tensor([_s64(int(x) & MASK64) for x in seeds], dtype=torch.int64,
+                        device=device)[:, None]
+    k = torch.arange(1, count + 1, dtype=torch.int64, device=device)[None, :]
+    z = s + k * _s64(GOLDEN)
+    z = (z ^ ((z >> 30) & ((1 << 34) - 1))) * _s64(MIX1)
+    z = (z ^ ((z >> 27) & ((1 << 37) - 1))) * _s64(MIX2)
+    return z ^ ((z >> 31) & ((1 << 33) - 1))
+
+
+def zipf_batch_device(seeds, g: int, skew: float, total_bytes: int, device, chunk: int = 32):
+    """[len(seeds), g, g] int64 on ``device``; equal to stacking
+    ``zipf_sizes(seed, g, skew, total_bytes)`` (the base shares do not depend
+    on the seed, only the stable argsort of the seed's stream does)."""
+    import torch
+
+    pairs = g * g - g
+    base = torch.from_numpy(_zipf_base(pairs, skew, int(total_bytes))).to(device)
+    offdiag = torch.from_numpy(np.flatnonzero(~np.eye(g, dtype=bool).ravel())).to(device)
+    seeds = list(seeds)
+    out = torch.zeros((len(seeds), g * g), dtype=torch.int64, device=device)
+    for c0 in range(0, len(seeds), chunk):
+        cs = seeds[c0:c0 + chunk]
+        keys = stream_device(cs, pairs, device) ^ _s64(1 << 63)  # unsigned order
+        order = torch.sort(keys, dim=1, stable=True).indices
+        out[c0:c0 + len(cs)].scatter_(1, offdiag[order], base.expand(len(cs), pairs))
+    return out.view(len(seeds), g, g)
+
+
 def gen_zipf(seed: int, t: Topology, skew: float, total_bytes: int) -> DemandMatrix:
     if not skew >= 0.0:
         raise ValidationError("skew must be >= 0")
