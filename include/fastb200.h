@@ -104,6 +104,116 @@ int fast_balance_batch(const int64_t *D, int B, int n, int m,
 int fast_decompose_batch(const int64_t *S, int B, int n, int mode,
                          const fast_sched_bufs *out, void *stream);
 
+/* ------------------------------------------------------------------------
+ * Executor: P2P stage execution over NVSwitch (replaces the reference's
+ * analytical "executor" simulate_fast, simulate.py:107-193, with real data
+ * movement; the paper's transfer engine is PAPER.md:605-619).
+ * ------------------------------------------------------------------------ */
+
+/* op phases, in execution-priority order */
+#define FAST_PH_BALANCE 0      /* giver -> taker staging (balance.py:77-126) */
+#define FAST_PH_DIRECT 1       /* intra tile, or stage send of own bytes     */
+#define FAST_PH_FROM_STAGING 2 /* stage send of balanced-in bytes           */
+#define FAST_PH_REDIST 3       /* proxy staging -> final GPU (balance.py:210)*/
+#define FAST_BUF_SEND 0
+#define FAST_BUF_RECV 1
+#define FAST_BUF_STAGING 2
+
+/* One byte-range copy executed by `exec_rank` into `dst_rank`'s buffer. */
+typedef struct {
+  int64_t src_off;
+  int64_t dst_off;
+  int64_t len;
+  int16_t exec_rank;
+  int16_t dst_rank;
+  uint8_t src_buf;
+  uint8_t dst_buf;
+  uint8_t phase;
+  uint8_t stage; /* position in the ascending stage order */
+} fast_op;
+
+/* Compiled plan buffers (device pointers, caller-owned). */
+typedef struct {
+  fast_op *ops;          /* [op_capacity] */
+  int32_t *n_ops;        /* [1] */
+  int64_t *staging_used; /* [G] staging bytes needed per rank */
+  int32_t *status;       /* [1] */
+  void *workspace;       /* fast_plan_workspace_bytes(n, m) */
+  int64_t op_capacity;
+} fast_plan;
+
+size_t fast_plan_workspace_bytes(int n, int m);
+int64_t fast_plan_op_capacity(int n, int m);
+
+/* Plan compile on the device (one-thread kernel, stream-ordered): D [G][G]
+ * and the packed schedule of matrix 0 of `sched` -> phase-ordered ops. */
+int fast_plan_compile(const int64_t *D, int n, int m,
+                      const fast_sched_bufs *sched, int64_t recv_capacity,
+                      int64_t staging_capacity, const fast_plan *plan,
+                      void *stream);
+
+/* Same plan logic on HOST pointers -- validation/inspection only (CPU
+ * tests); the executor never calls it.  `order/perm/sbytes` are one
+ * matrix's packed stage arrays, K = n*n-2n+2. */
+int fast_plan_compile_host(const int64_t *D, int n, int m, int n_stages,
+                           const int32_t *order, const uint8_t *perm,
+                           const int64_t *sbytes, int64_t recv_capacity,
+                           int64_t staging_capacity, fast_op *ops,
+                           int64_t op_capacity, int32_t *n_ops,
+                           int64_t *staging_used, void *workspace);
+
+/* Communicator: one process per GPU; each rank owns one symmetric
+ * allocation [flags | demand x2 | recv | staging] exported by CUDA IPC. */
+typedef struct fast_comm fast_comm;
+
+int fast_comm_create(int rank, int world, int max_gpus_per_row,
+                     int64_t recv_bytes, int64_t staging_bytes,
+                     fast_comm **out);
+/* 64-byte cudaIpcMemHandle_t of this rank's symmetric allocation. */
+int fast_comm_ipc_handle(const fast_comm *c, void *handle64);
+/* handles: world x 64 bytes gathered from every rank (own entry ignored). */
+int fast_comm_open_peers(fast_comm *c, const void *handles);
+int fast_comm_destroy(fast_comm *c);
+void *fast_comm_recv_ptr(const fast_comm *c);
+void *fast_comm_staging_ptr(const fast_comm *c);
+/* demand-matrix buffer of call `epoch` (double-buffered by parity) */
+int64_t *fast_comm_demand_ptr(const fast_comm *c, int64_t epoch);
+int64_t fast_comm_recv_capacity(const fast_comm *c);
+int64_t fast_comm_staging_capacity(const fast_comm *c);
+
+/* All-gather of this rank's demand row (int64[world], device) into every
+ * rank's demand buffer for `epoch` (>= 1, +1 per call): P2P writes + a
+ * release counter; returns after the local matrix is complete (on the
+ * device, stream-ordered).  Replaces Megatron's count all-gather
+ * (PAPER.md:617-619). */
+int fast_gather_demand(fast_comm *c, const int64_t *row, int64_t epoch,
+                       void *stream);
+
+/* Execute a compiled plan: one persistent kernel per rank (`blocks` CTAs);
+ * entry barrier, then balance pushes, intra copies and stage sends, then
+ * redistribution, all chunked (`chunk_bytes`) and flag-synchronised.
+ * On return (stream order) the local recv buffer holds the alltoallv
+ * result.  timeline_ns (device int64[8 + 2*256] or NULL) receives
+ * %globaltimer stamps: [0] start, [1] barrier passed, [2] balance arrivals
+ * complete, [3] own ops done, [4] recv complete, [8+k] stage k arrivals at
+ * this proxy complete. */
+int fast_exec(fast_comm *c, const fast_plan *plan, const void *send,
+              int64_t epoch, int blocks, int64_t chunk_bytes,
+              int64_t *timeline_ns, void *stream);
+/* One-GPU group mode (testing the full protocol on a single device): `world`
+ * communicators whose symmetric blocks all live on the current device, and
+ * one cooperative launch (grid = blocks x world, all CTAs co-resident) that
+ * runs every rank's part of the plan.  sends: host array of `world` device
+ * pointers.  timeline_ns: world x (8+256) int64 or NULL. */
+int fast_comm_create_group(int world, int64_t recv_bytes, int64_t staging_bytes,
+                           fast_comm **comms);
+int fast_exec_group(fast_comm *const *comms, int world, const fast_plan *plan,
+                    const void *const *sends, int64_t epoch, int blocks,
+                    int64_t chunk_bytes, int64_t *timeline_ns, void *stream);
+/* Device status word of the last exec on this comm (0 ok, 3 = a wait timed
+ * out: peers missing or protocol error). */
+int fast_comm_status(const fast_comm *c, int32_t *status_host);
+
 #ifdef __cplusplus
 }
 #endif

@@ -4,4 +4,33 @@ from __future__ import annotations
 
 import ctypes
 
-SIGNATURES: list[tuple[str, object, list]] = []
+from ._lib import FastPlan, FastSchedBufs
+
+V = ctypes.c_void_p
+I = ctypes.c_int
+I64 = ctypes.c_int64
+P_SCHED = ctypes.POINTER(FastSchedBufs)
+P_PLAN = ctypes.POINTER(FastPlan)
+
+SIGNATURES: list[tuple[str, object, list]] = [
+    # executor: plan compile (exec.cu / plan.cuh)
+    ("fast_plan_workspace_bytes", ctypes.c_size_t, [I, I]),
+    ("fast_plan_op_capacity", I64, [I, I]),
+    ("fast_plan_compile", I, [V, I, I, P_SCHED, I64, I64, P_PLAN, V]),
+    ("fast_plan_compile_host", I, [V, I, I, I, V, V, V, I64, I64, V, I64, V, V, V]),
+    # communicator + P2P execution
+    ("fast_comm_create", I, [I, I, I, I64, I64, ctypes.POINTER(V)]),
+    ("fast_comm_ipc_handle", I, [V, V]),
+    ("fast_comm_open_peers", I, [V, ctypes.c_char_p]),
+    ("fast_comm_destroy", I, [V]),
+    ("fast_comm_recv_ptr", V, [V]),
+    ("fast_comm_staging_ptr", V, [V]),
+    ("fast_comm_demand_ptr", V, [V, I64]),
+    ("fast_comm_recv_capacity", I64, [V]),
+    ("fast_comm_staging_capacity", I64, [V]),
+    ("fast_gather_demand", I, [V, V, I64, V]),
+    ("fast_exec", I, [V, P_PLAN, V, I64, I, I64, V, V]),
+    ("fast_comm_status", I, [V, ctypes.POINTER(ctypes.c_int32)]),
+    ("fast_comm_create_group", I, [I, I64, I64, ctypes.POINTER(V)]),
+    ("fast_exec_group", I, [ctypes.POINTER(V), I, P_PLAN, ctypes.POINTER(V), I64, I, I64, V, V]),
+]

@@ -39,6 +39,14 @@ class FastSchedBufs(ctypes.Structure):
         "stage_order", "status", "workspace")]
 
 
+class FastPlan(ctypes.Structure):
+    """Mirror of ``fast_plan`` (device pointers + capacity)."""
+
+    _fields_ = [("ops", ctypes.c_void_p), ("n_ops", ctypes.c_void_p),
+                ("staging_used", ctypes.c_void_p), ("status", ctypes.c_void_p),
+                ("workspace", ctypes.c_void_p), ("op_capacity", ctypes.c_int64)]
+
+
 # (name, restype, argtypes) of every exported entry point; the CPU test
 # suite checks that each one is present in the built library.
 SIGNATURES: list[tuple[str, object, list]] = [
@@ -74,13 +82,14 @@ def load() -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
+    path = os.environ.get("FASTB200_LIB", LIB_PATH)  # experiment builds only
+    if path == LIB_PATH and not os.path.exists(LIB_PATH):
         from ._build import build
 
         build()
-    if not os.path.exists(LIB_PATH):
-        raise RuntimeError(f"libfastb200.so missing at {LIB_PATH}: run build()")
-    lib = ctypes.CDLL(LIB_PATH)
+    if not os.path.exists(path):
+        raise RuntimeError(f"libfastb200.so missing at {path}: run build()")
+    lib = ctypes.CDLL(path)
     for name, res, args in SIGNATURES + extra_signatures():
         fn = getattr(lib, name, None)
         if fn is None:

@@ -1,0 +1,559 @@
+// exec.cu -- FAST stage execution over NVLink 5 / NVSwitch (sm_100a).
+//
+// One process per GPU.  Every rank owns ONE symmetric allocation exported
+// with CUDA IPC and mapped by every peer:
+//
+//   [0, 4 KiB)          flags: u64 counters (see CTR_*), peers add to them
+//   [4 KiB, +2*G*G*8)   demand matrix, double-buffered by call parity
+//   recv region         alltoallv result (source-major segments)
+//   staging region      balanced-in bytes and proxy-held redistribution bytes
+//
+// Kernels (all stream-ordered on the caller's stream, no host round trip):
+//   gather_demand_kernel  P2P all-gather of the per-rank demand rows
+//   plan_kernel           plan_compile (plan.cuh) in one device thread
+//   exec_kernel           persistent, `blocks` CTAs per rank: entry barrier,
+//                         then the rank's ops in phase order, chunked, each
+//                         chunk a 16-byte-vectorised copy into peer HBM
+//                         followed by a release-add on the consumer's counter;
+//                         consumers acquire before reading staging.
+//
+// Deadlock freedom: ops are emitted in phase order (balance < direct <
+// from-staging < redistribution) and every wait targets an earlier phase, so
+// with all CTAs of all ranks co-resident (grid <= SM count) every wait is
+// eventually satisfied.  Every wait is bounded by a timeout that records
+// status 3 instead of hanging the device.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "fastb200.h"
+#include "plan.cuh"
+
+namespace {
+
+constexpr int64_t kFlagBytes = 4096;
+constexpr int CTR_ARRIVE = 0;   // entry barrier, monotonic (+1 per peer/call)
+constexpr int CTR_GO = 1;       // local: barrier passed for epoch
+constexpr int CTR_BAL = 2;      // balance chunks landed in my staging
+constexpr int CTR_RECV = 3;     // chunks landed in my recv
+constexpr int CTR_GATHER = 4;   // demand rows landed (monotonic)
+constexpr int CTR_STATUS = 5;   // local error word
+constexpr int CTR_STAGE = 8;    // + k: stage-k chunks landed in my staging
+constexpr int kMaxStages = 256;
+constexpr int kExecThreads = 512;
+constexpr long long kSpinLimitNs = 20LL * 1000 * 1000 * 1000;  // 20 s
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_sys_add(uint64_t* p, uint64_t v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Spin until *p >= target (acquire, system scope).  false on timeout.
+__device__ bool wait_geq(const uint64_t* p, uint64_t target, bool sys) {
+  const uint64_t t0 = globaltimer();
+  int spins = 0;
+  for (;;) {
+    const uint64_t v = sys ? ld_acquire_sys(p) : ld_acquire_gpu(p);
+    if (v >= target) return true;
+    if (++spins > 64) {
+      __nanosleep(128);
+      if ((int64_t)(globaltimer() - t0) > kSpinLimitNs) return false;
+    }
+  }
+}
+
+constexpr int kMaxRanks = 16;       // one NVSwitch node
+constexpr int kTimelineStride = 8 + kMaxStages;
+
+struct ExecArgs {
+  uint8_t* const* peers;  // [world] base of every rank's symmetric block
+  const fast_op* ops;
+  const int32_t* n_ops;
+  const int32_t* plan_status;
+  const uint8_t* sends[kMaxRanks];  // indexed by blockIdx.y (local rank slot)
+  const uint8_t* send;
+  int64_t recv_off, staging_off;  // region offsets inside a symmetric block
+  int64_t chunk;
+  int64_t epoch;
+  int64_t* timeline;
+  int rank, world;
+};
+
+__device__ __forceinline__ uint64_t* ctr(uint8_t* base, int idx) {
+  return reinterpret_cast<uint64_t*>(base) + idx;
+}
+
+// ---- CTA-wide byte copy, 16-byte vectorised on the destination ------------
+__device__ __forceinline__ uint4 ld16(const uint8_t* p, bool nc) {
+  uint4 v;
+  if (nc) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  } else {
+    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  }
+  return v;
+}
+__device__ __forceinline__ void st16(uint8_t* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// Extract 16 bytes starting `sh` (1..15) bytes into the 32-byte window a:b.
+__device__ __forceinline__ uint4 shift_window(const uint4 a, const uint4 b, int sh) {
+  const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  const int ws = sh >> 2, bs = (sh & 3) * 8;
+  uint32_t o[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (ws == c) { lo = w[c + j]; hi = w[c + j + 1]; }
+    o[j] = __funnelshift_r(lo, hi, bs);
+  }
+  return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+__device__ void cta_copy(uint8_t* dst, const uint8_t* src, int64_t len, bool nc) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  int64_t head = (16 - ((uintptr_t)dst & 15)) & 15;
+  if (head > len) head = len;
+  if (tid < head) dst[tid] = src[tid];
+  dst += head;
+  src += head;
+  len -= head;
+  const int64_t nw = len >> 4;
+  const int sh = (int)((uintptr_t)src & 15);
+  constexpr int U = 4;
+  if (sh == 0) {
+    int64_t wi = tid;
+    for (; wi + (U - 1) * nt < nw; wi += U * nt) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ld16(src + (wi + u * nt) * 16, nc);
+#pragma unroll
+      for (int u = 0; u < U; ++u) st16(dst + (wi + u * nt) * 16, v[u]);
+    }
+    for (; wi < nw; wi += nt) st16(dst + wi * 16, ld16(src + wi * 16, nc));
+  } else {
+    const uint8_t* sa = src - sh;  // 16-byte aligned
+    int64_t wi = tid;
+    for (; wi + (U - 1) * nt < nw; wi += U * nt) {
+      uint4 a[U], b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        a[u] = ld16(sa + (wi + u * nt) * 16, nc);
+        b[u] = ld16(sa + (wi + u * nt) * 16 + 16, nc);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) st16(dst + (wi + u * nt) * 16, shift_window(a[u], b[u], sh));
+    }
+    for (; wi < nw; wi += nt)
+      st16(dst + wi * 16, shift_window(ld16(sa + wi * 16, nc), ld16(sa + wi * 16 + 16, nc), sh));
+  }
+  const int64_t tail = len - nw * 16;
+  if (tid < tail) dst[nw * 16 + tid] = src[nw * 16 + tid];
+}
+
+// ---- kernels ----------------------------------------------------------------
+
+__global__ void gather_demand_kernel(uint8_t* const* peers, const int64_t* row,
+                                     int64_t epoch, int rank, int world,
+                                     int64_t demand_off) {
+  // lane r (< world) writes this rank's row into rank r's demand buffer
+  const int G = world;
+  const int par = (int)(epoch & 1);
+  for (int r = threadIdx.x; r < world; r += blockDim.x) {
+    int64_t* dm = reinterpret_cast<int64_t*>(peers[r] + demand_off) + (int64_t)par * G * G;
+    for (int h = 0; h < G; ++h) dm[(int64_t)rank * G + h] = row[h];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int r = 0; r < world; ++r) red_release_sys_add(ctr(peers[r], CTR_GATHER), 1);
+    if (!wait_geq(ctr(peers[rank], CTR_GATHER), (uint64_t)epoch * world, true))
+      atomicExch(reinterpret_cast<unsigned long long*>(ctr(peers[rank], CTR_STATUS)), 3ull);
+  }
+}
+
+__device__ __forceinline__ int64_t nchunks(int64_t len, int64_t chunk) {
+  return (len + chunk - 1) / chunk;
+}
+
+// grid (blocks, ranks_in_launch): blockIdx.y selects the rank this CTA acts
+// for -- 1 in the multi-process mode, all `world` ranks in the one-GPU group
+// mode (cooperative launch, so every rank's CTAs are co-resident).
+__global__ void __launch_bounds__(kExecThreads) exec_kernel(ExecArgs a) {
+  __shared__ int64_t s_exp[3 + kMaxStages];  // bal, recv, (unused), stage k
+  __shared__ int s_fail;
+  a.rank += blockIdx.y;
+  a.send = a.sends[blockIdx.y];
+  if (a.timeline) a.timeline += (int64_t)blockIdx.y * kTimelineStride;
+  uint8_t* me = a.peers[a.rank];
+  uint64_t* status = ctr(me, CTR_STATUS);
+  const int tid = threadIdx.x;
+  if (tid == 0) s_fail = 0;
+
+  // ---- entry barrier (CTA 0): reset own counters, then arrive everywhere --
+  if (blockIdx.x == 0 && tid == 0) {
+    if (a.timeline) a.timeline[0] = (int64_t)globaltimer();
+    volatile uint64_t* c = reinterpret_cast<volatile uint64_t*>(me);
+    c[CTR_BAL] = 0;
+    c[CTR_RECV] = 0;
+    for (int k = 0; k < kMaxStages; ++k) c[CTR_STAGE + k] = 0;
+    __threadfence_system();
+    for (int r = 0; r < a.world; ++r)
+      if (r != a.rank) red_release_sys_add(ctr(a.peers[r], CTR_ARRIVE), 1);
+    if (!wait_geq(ctr(me, CTR_ARRIVE), (uint64_t)a.epoch * (a.world - 1), true)) s_fail = 1;
+    st_release_gpu(ctr(me, CTR_GO), (uint64_t)a.epoch);
+    if (a.timeline) a.timeline[1] = (int64_t)globaltimer();
+  } else if (tid == 0) {
+    if (!wait_geq(ctr(me, CTR_GO), (uint64_t)a.epoch, false)) s_fail = 1;
+  }
+  // expected arrivals into this rank, from the global op list
+  for (int i = tid; i < 3 + kMaxStages; i += blockDim.x) s_exp[i] = 0;
+  __syncthreads();
+  const int nops = (*a.plan_status == FAST_OK) ? *a.n_ops : 0;
+  for (int i = tid; i < nops; i += blockDim.x) {
+    const fast_op o = a.ops[i];
+    if (o.dst_rank != a.rank) continue;
+    const int64_t nc = nchunks(o.len, a.chunk);
+    if (o.dst_buf == FAST_BUF_RECV) atomicAdd((unsigned long long*)&s_exp[1], (unsigned long long)nc);
+    else if (o.phase == FAST_PH_BALANCE) atomicAdd((unsigned long long*)&s_exp[0], (unsigned long long)nc);
+    else atomicAdd((unsigned long long*)&s_exp[3 + o.stage], (unsigned long long)nc);
+  }
+  __syncthreads();
+
+  // ---- my ops, phase-ordered, chunks dealt round-robin over CTAs ----------
+  int64_t item = 0;
+  bool bal_ready = false;
+  for (int i = 0; i < nops && !s_fail; ++i) {
+    const fast_op o = a.ops[i];
+    if (o.exec_rank != a.rank) continue;
+    const int64_t nc = nchunks(o.len, a.chunk);
+    int64_t c = ((int64_t)blockIdx.x - item) % gridDim.x;
+    if (c < 0) c += gridDim.x;
+    item += nc;
+    if (c >= nc) continue;
+    // wait for this op's inputs (once per op per CTA)
+    if (o.phase == FAST_PH_FROM_STAGING && !bal_ready) {
+      if (tid == 0 && !wait_geq(ctr(me, CTR_BAL), (uint64_t)s_exp[0], true)) s_fail = 1;
+      bal_ready = true;
+      if (blockIdx.x == 0 && tid == 0 && a.timeline) a.timeline[2] = (int64_t)globaltimer();
+    } else if (o.phase == FAST_PH_REDIST) {
+      if (tid == 0 && !wait_geq(ctr(me, CTR_STAGE + o.stage), (uint64_t)s_exp[3 + o.stage], true))
+        s_fail = 1;
+    }
+    __syncthreads();
+    if (s_fail) break;
+    const uint8_t* src = (o.src_buf == FAST_BUF_SEND ? a.send : me + a.staging_off) + o.src_off;
+    uint8_t* peer = a.peers[o.dst_rank];
+    uint8_t* dst = peer + (o.dst_buf == FAST_BUF_RECV ? a.recv_off : a.staging_off) + o.dst_off;
+    uint64_t* sig = ctr(peer, o.dst_buf == FAST_BUF_RECV ? CTR_RECV
+                              : o.phase == FAST_PH_BALANCE ? CTR_BAL : CTR_STAGE + o.stage);
+    const bool nc_ok = o.src_buf == FAST_BUF_SEND;
+    for (; c < nc; c += gridDim.x) {
+      const int64_t off = c * a.chunk;
+      const int64_t len = o.len - off < a.chunk ? o.len - off : a.chunk;
+      cta_copy(dst + off, src + off, len, nc_ok);
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence_system();
+        red_release_sys_add(sig, 1);
+      }
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && tid == 0) {
+    if (a.timeline) a.timeline[3] = (int64_t)globaltimer();
+    if (!s_fail && !wait_geq(ctr(me, CTR_RECV), (uint64_t)s_exp[1], true)) s_fail = 1;
+    if (a.timeline) a.timeline[4] = (int64_t)globaltimer();
+  }
+  __syncthreads();
+  if (tid == 0 && s_fail) atomicExch(reinterpret_cast<unsigned long long*>(status), 3ull);
+}
+
+// Device plan kernel: takes n_stages / synthesis status from device memory.
+__global__ void fast_plan_kernel_dev(fastplan::PlanIn in, fastplan::PlanOut out,
+                                     const int32_t* n_stages, const int32_t* sched_status) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (*sched_status != FAST_OK) {
+    *out.n_ops = 0;
+    *out.status = *sched_status;
+    return;
+  }
+  in.n_stages = *n_stages;
+  fastplan::plan_compile(in, out);
+}
+
+}  // namespace
+
+struct fast_comm {
+  int rank, world, gmax;
+  int64_t recv_bytes, staging_bytes;
+  int64_t demand_off, recv_off, staging_off, total;
+  uint8_t* base;             // own symmetric allocation
+  uint8_t** peers_host;      // [world]
+  uint8_t** peers_dev;       // [world] device copy
+  cudaIpcMemHandle_t handle;
+  int opened;
+};
+
+extern "C" {
+
+size_t fast_plan_workspace_bytes(int n, int m) {
+  return (size_t)fastplan::plan_ws_bytes(n, m);
+}
+
+int64_t fast_plan_op_capacity(int n, int m) {
+  return fastplan::plan_op_capacity(n, m, n * n - 2 * n + 2);
+}
+
+int fast_plan_compile(const int64_t* D, int n, int m, const fast_sched_bufs* sched,
+                      int64_t recv_capacity, int64_t staging_capacity,
+                      const fast_plan* plan, void* stream) {
+  if (!sched || !plan || n < 2 || m < 1 || m > FAST_MAX_GPUS_PER_SERVER) return FAST_EVALIDATION;
+  fastplan::PlanIn in;
+  in.n = n;
+  in.m = m;
+  in.K = n * n - 2 * n + 2;
+  in.D = D;
+  in.n_stages = -1;  // read on the device
+  in.order = sched->stage_order;
+  in.perm = sched->stage_perm;
+  in.sbytes = sched->stage_bytes;
+  in.recv_cap = recv_capacity;
+  in.staging_cap = staging_capacity;
+  in.op_cap = plan->op_capacity;
+  fastplan::PlanOut out;
+  out.ops = plan->ops;
+  out.n_ops = plan->n_ops;
+  out.staging_used = plan->staging_used;
+  out.status = plan->status;
+  out.ws = plan->workspace;
+  fast_plan_kernel_dev<<<1, 32, 0, (cudaStream_t)stream>>>(in, out, sched->n_stages,
+                                                           sched->status);
+  return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
+}
+
+int fast_plan_compile_host(const int64_t* D, int n, int m, int n_stages, const int32_t* order,
+                           const uint8_t* perm, const int64_t* sbytes, int64_t recv_capacity,
+                           int64_t staging_capacity, fast_op* ops, int64_t op_capacity,
+                           int32_t* n_ops, int64_t* staging_used, void* workspace) {
+  if (n < 2 || m < 1 || m > FAST_MAX_GPUS_PER_SERVER || !D || !ops || !workspace)
+    return FAST_EVALIDATION;
+  fastplan::PlanIn in;
+  in.n = n;
+  in.m = m;
+  in.K = n * n - 2 * n + 2;
+  in.D = D;
+  in.n_stages = n_stages;
+  in.order = order;
+  in.perm = perm;
+  in.sbytes = sbytes;
+  in.recv_cap = recv_capacity;
+  in.staging_cap = staging_capacity;
+  in.op_cap = op_capacity;
+  int32_t status = 0;
+  fastplan::PlanOut out;
+  out.ops = ops;
+  out.n_ops = n_ops;
+  out.staging_used = staging_used;
+  out.status = &status;
+  out.ws = workspace;
+  fastplan::plan_compile(in, out);
+  return status;
+}
+
+int fast_comm_create(int rank, int world, int max_gpus_per_row, int64_t recv_bytes,
+                     int64_t staging_bytes, fast_comm** out) {
+  (void)max_gpus_per_row;
+  if (!out || world < 1 || rank < 0 || rank >= world || recv_bytes < 0 || staging_bytes < 0)
+    return FAST_EVALIDATION;
+  fast_comm* c = (fast_comm*)calloc(1, sizeof(fast_comm));
+  if (!c) return FAST_ECUDA;
+  c->rank = rank;
+  c->world = world;
+  c->recv_bytes = recv_bytes;
+  c->staging_bytes = staging_bytes;
+  c->demand_off = kFlagBytes;
+  c->recv_off = fastplan::align16(c->demand_off + 2 * (int64_t)world * world * 8 + 256);
+  c->recv_off = (c->recv_off + 4095) & ~(int64_t)4095;
+  c->staging_off = (c->recv_off + recv_bytes + 64 + 4095) & ~(int64_t)4095;
+  c->total = (c->staging_off + staging_bytes + 64 + 4095) & ~(int64_t)4095;
+  if (cudaMalloc(&c->base, (size_t)c->total) != cudaSuccess) { free(c); return FAST_ECUDA; }
+  if (cudaMemset(c->base, 0, (size_t)kFlagBytes + 2 * (size_t)world * world * 8) != cudaSuccess ||
+      cudaIpcGetMemHandle(&c->handle, c->base) != cudaSuccess) {
+    cudaFree(c->base);
+    free(c);
+    return FAST_ECUDA;
+  }
+  c->peers_host = (uint8_t**)calloc(world, sizeof(uint8_t*));
+  c->peers_host[rank] = c->base;
+  if (cudaMalloc(&c->peers_dev, sizeof(uint8_t*) * world) != cudaSuccess) {
+    cudaFree(c->base);
+    free(c->peers_host);
+    free(c);
+    return FAST_ECUDA;
+  }
+  cudaDeviceSynchronize();
+  *out = c;
+  return FAST_OK;
+}
+
+int fast_comm_ipc_handle(const fast_comm* c, void* handle64) {
+  if (!c || !handle64) return FAST_EVALIDATION;
+  memcpy(handle64, &c->handle, sizeof(cudaIpcMemHandle_t));
+  return FAST_OK;
+}
+
+int fast_comm_open_peers(fast_comm* c, const void* handles) {
+  if (!c || !handles) return FAST_EVALIDATION;
+  const uint8_t* h = (const uint8_t*)handles;
+  for (int r = 0; r < c->world; ++r) {
+    if (r == c->rank) continue;
+    cudaIpcMemHandle_t hd;
+    memcpy(&hd, h + (size_t)r * 64, sizeof(hd));
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+      return FAST_ECUDA;
+    c->peers_host[r] = (uint8_t*)p;
+  }
+  if (cudaMemcpy(c->peers_dev, c->peers_host, sizeof(uint8_t*) * c->world,
+                 cudaMemcpyHostToDevice) != cudaSuccess)
+    return FAST_ECUDA;
+  c->opened = 1;
+  return FAST_OK;
+}
+
+int fast_comm_destroy(fast_comm* c) {
+  if (!c) return FAST_OK;
+  cudaDeviceSynchronize();
+  if (c->opened == 1)
+    for (int r = 0; r < c->world; ++r)
+      if (r != c->rank && c->peers_host[r]) cudaIpcCloseMemHandle(c->peers_host[r]);
+  cudaFree(c->peers_dev);
+  cudaFree(c->base);
+  free(c->peers_host);
+  free(c);
+  return FAST_OK;
+}
+
+void* fast_comm_recv_ptr(const fast_comm* c) { return c ? c->base + c->recv_off : nullptr; }
+void* fast_comm_staging_ptr(const fast_comm* c) { return c ? c->base + c->staging_off : nullptr; }
+int64_t* fast_comm_demand_ptr(const fast_comm* c, int64_t epoch) {
+  if (!c) return nullptr;
+  return reinterpret_cast<int64_t*>(c->base + c->demand_off) +
+         (epoch & 1) * (int64_t)c->world * c->world;
+}
+int64_t fast_comm_recv_capacity(const fast_comm* c) { return c ? c->recv_bytes : 0; }
+int64_t fast_comm_staging_capacity(const fast_comm* c) { return c ? c->staging_bytes : 0; }
+
+int fast_gather_demand(fast_comm* c, const int64_t* row, int64_t epoch, void* stream) {
+  if (!c || !c->opened || !row || epoch < 1) return FAST_EVALIDATION;
+  gather_demand_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(c->peers_dev, row, epoch, c->rank,
+                                                           c->world, c->demand_off);
+  return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
+}
+
+int fast_exec(fast_comm* c, const fast_plan* plan, const void* send, int64_t epoch, int blocks,
+              int64_t chunk_bytes, int64_t* timeline_ns, void* stream) {
+  if (!c || !c->opened || !plan || epoch < 1 || blocks < 1 || chunk_bytes < 16)
+    return FAST_EVALIDATION;
+  ExecArgs a;
+  memset(&a, 0, sizeof(a));
+  a.peers = c->peers_dev;
+  a.ops = plan->ops;
+  a.n_ops = plan->n_ops;
+  a.plan_status = plan->status;
+  a.sends[0] = (const uint8_t*)send;
+  a.recv_off = c->recv_off;
+  a.staging_off = c->staging_off;
+  a.chunk = chunk_bytes & ~(int64_t)15;
+  a.epoch = epoch;
+  a.timeline = timeline_ns;
+  a.rank = c->rank;
+  a.world = c->world;
+  exec_kernel<<<blocks, kExecThreads, 0, (cudaStream_t)stream>>>(a);
+  return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
+}
+
+int fast_comm_create_group(int world, int64_t recv_bytes, int64_t staging_bytes,
+                           fast_comm** comms) {
+  if (!comms || world < 1 || world > kMaxRanks) return FAST_EVALIDATION;
+  for (int r = 0; r < world; ++r) {
+    int rc = fast_comm_create(r, world, 0, recv_bytes, staging_bytes, &comms[r]);
+    if (rc != FAST_OK) {
+      for (int q = 0; q < r; ++q) fast_comm_destroy(comms[q]);
+      return rc;
+    }
+  }
+  for (int r = 0; r < world; ++r) {
+    for (int q = 0; q < world; ++q) comms[r]->peers_host[q] = comms[q]->base;
+    if (cudaMemcpy(comms[r]->peers_dev, comms[r]->peers_host, sizeof(uint8_t*) * world,
+                   cudaMemcpyHostToDevice) != cudaSuccess)
+      return FAST_ECUDA;
+    comms[r]->opened = 2;  // group member: peers are local allocations
+  }
+  return FAST_OK;
+}
+
+int fast_exec_group(fast_comm* const* comms, int world, const fast_plan* plan,
+                    const void* const* sends, int64_t epoch, int blocks,
+                    int64_t chunk_bytes, int64_t* timeline_ns, void* stream) {
+  if (!comms || world < 1 || world > kMaxRanks || !plan || epoch < 1 || blocks < 1 ||
+      chunk_bytes < 16)
+    return FAST_EVALIDATION;
+  ExecArgs a;
+  memset(&a, 0, sizeof(a));
+  a.peers = comms[0]->peers_dev;
+  a.ops = plan->ops;
+  a.n_ops = plan->n_ops;
+  a.plan_status = plan->status;
+  for (int r = 0; r < world; ++r) a.sends[r] = (const uint8_t*)sends[r];
+  a.recv_off = comms[0]->recv_off;
+  a.staging_off = comms[0]->staging_off;
+  a.chunk = chunk_bytes & ~(int64_t)15;
+  a.epoch = epoch;
+  a.timeline = timeline_ns;
+  a.rank = 0;
+  a.world = world;
+  void* args[] = {&a};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)exec_kernel, dim3(blocks, world),
+                                              dim3(kExecThreads), args, 0,
+                                              (cudaStream_t)stream);
+  return e == cudaSuccess ? FAST_OK : FAST_ECUDA;
+}
+
+int fast_comm_status(const fast_comm* c, int32_t* status_host) {
+  if (!c || !status_host) return FAST_EVALIDATION;
+  uint64_t v = 0;
+  if (cudaMemcpy(&v, c->base + CTR_STATUS * 8, 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return FAST_ECUDA;
+  *status_host = (int32_t)v;
+  return FAST_OK;
+}
+
+}  // extern "C"
+

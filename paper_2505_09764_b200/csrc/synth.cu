@@ -29,8 +29,11 @@
 
 namespace {
 
-constexpr int kBalThreads = 128;
+constexpr int kBalThreads = 256;
 constexpr int kDecWarps = 4;  // matrices per CTA in decompose_kernel
+#ifndef FAST_DFS_ALL_LANES
+#define FAST_DFS_ALL_LANES 0
+#endif
 constexpr int64_t kMaxSafeTotal = int64_t(1) << 62;  // model.py:26
 
 __device__ __forceinline__ int64_t sat_add(int64_t s, int64_t v) {
@@ -117,6 +120,51 @@ __device__ int balance_tile(int64_t* __restrict__ t, const int m_rt,
 }
 
 // grid (n, ceil(n/J), B), block kBalThreads, dyn smem J*(m*m+1)*8.
+// Stage-in/out walk the strip row by row (no integer division by a runtime
+// value); even m moves 16-byte pairs (rows of a G x G int64 matrix with G
+// even are 16-byte aligned), odd m single words.
+template <int M>
+__device__ __forceinline__ void strip_rows(int64_t* __restrict__ sm,
+                                           const int64_t* __restrict__ g_in,
+                                           int64_t* __restrict__ g_out,
+                                           const int m_rt, const int64_t G,
+                                           const int Jc, const bool load) {
+  const int m = M ? M : m_rt;
+  const int TS = m * m + 1;
+  const int cols = Jc * m;
+  if ((M ? (M % 2 == 0) : (m % 2 == 0))) {
+    const int pairs = cols >> 1;
+    for (int r = 0; r < m; ++r) {
+      const int64_t rowoff = (int64_t)r * G;
+      for (int e = threadIdx.x; e < pairs; e += blockDim.x) {
+        const int col = 2 * e;
+        const int jj = col / m, c = col - jj * m;
+        int64_t* sp = sm + jj * TS + r * m + c;
+        if (load) {
+          const longlong2 x = __ldcs(reinterpret_cast<const longlong2*>(g_in + rowoff + col));
+          sp[0] = x.x;
+          sp[1] = x.y;
+        } else {
+          longlong2 x;
+          x.x = sp[0];
+          x.y = sp[1];
+          __stcs(reinterpret_cast<longlong2*>(g_out + rowoff + col), x);
+        }
+      }
+    }
+  } else {
+    for (int r = 0; r < m; ++r) {
+      const int64_t rowoff = (int64_t)r * G;
+      for (int col = threadIdx.x; col < cols; col += blockDim.x) {
+        const int jj = col / m, c = col - jj * m;
+        int64_t* sp = sm + jj * TS + r * m + c;
+        if (load) *sp = __ldcs(g_in + rowoff + col);
+        else __stcs(g_out + rowoff + col, *sp);
+      }
+    }
+  }
+}
+
 template <int M>
 __global__ void __launch_bounds__(kBalThreads)
     balance_kernel(const int64_t* __restrict__ D, const int n, const int m_rt,
@@ -127,18 +175,10 @@ __global__ void __launch_bounds__(kBalThreads)
   const int Jc = min(J, n - j0);
   const int64_t G = (int64_t)n * m;
   const int TS = m * m + 1;  // +1 word of padding per tile (bank spread)
-  const int cols = Jc * m;
-  const int total = m * cols;
   const int64_t* Db = D + (int64_t)b * G * G + (int64_t)i * m * G + j0 * m;
   int64_t* Bb = out.balanced + (int64_t)b * G * G + (int64_t)i * m * G + j0 * m;
 
-  // Coalesced stage-in of the m x (Jc*m) strip, scattered into tile-major
-  // shared memory.
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int r = idx / cols, col = idx - r * cols;
-    const int jj = col / m, c = col - jj * m;
-    sm[jj * TS + r * m + c] = __ldcs(Db + (int64_t)r * G + col);
-  }
+  strip_rows<M>(sm, Db, nullptr, m, G, Jc, true);
   __syncthreads();
 
   if (threadIdx.x < Jc) {
@@ -147,11 +187,13 @@ __global__ void __launch_bounds__(kBalThreads)
     int32_t* st = out.status + b;
     bool bad = false;
     int64_t s = 0;
-    for (int k = 0; k < m * m; ++k) {
-      const int64_t v = t[k];
-      if (v < 0) { bad = true; continue; }
-      if (i == j && (k / m) == (k % m) && v != 0) bad = true;
-      s = sat_add(s, v);
+    for (int p = 0; p < m; ++p) {
+      for (int q = 0; q < m; ++q) {
+        const int64_t v = t[p * m + q];
+        if (v < 0) { bad = true; continue; }
+        if (i == j && p == q && v != 0) bad = true;
+        s = sat_add(s, v);
+      }
     }
     out.server[(int64_t)b * n * n + i * n + j] = s;
     if (bad) {
@@ -182,102 +224,10 @@ __global__ void __launch_bounds__(kBalThreads)
     }
   }
   __syncthreads();
-
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int r = idx / cols, col = idx - r * cols;
-    const int jj = col / m, c = col - jj * m;
-    __stcs(Bb + (int64_t)r * G + col, sm[jj * TS + r * m + c]);
-  }
+  strip_rows<M>(sm, nullptr, Bb, m, G, Jc, false);
 }
 
 // ---------------------------------------------------------------------------
-// Decomposition: one warp per matrix.
-
-struct DecSmem {
-  int64_t* mv;    // [n] work value of each row's matched cell
-  int64_t* am;    // [n] aux_left of each row's matched cell
-  int64_t* R;     // [n+1] prefix of row deficits (embedding)
-  int64_t* C;     // [n+1] prefix of column deficits
-  uint32_t* sup;  // [n][W] support bitset: work[u][v] > 0
-  uint32_t* seen; // [W]
-  int16_t* rm;    // [n] row_match
-  int16_t* cm;    // [n] col_match
-  int16_t* snap;  // [n] row_match before re-augmentation
-  int16_t* su;    // [n] DFS stack: row
-  int16_t* sv;    // [n] DFS stack: column taken by that row
-  int16_t* freed; // [n]
-};
-
-__host__ __device__ __forceinline__ size_t dec_smem_bytes(int n) {
-  const int W = (n + 31) / 32;
-  size_t b = 0;
-  b += 2 * (size_t)n * 8;            // mv, am
-  b += 2 * (size_t)(n + 1) * 8;      // R, C
-  b += (size_t)n * W * 4 + W * 4;    // sup, seen
-  b += 6 * (size_t)n * 2;            // rm cm snap su sv freed
-  return (b + 15) & ~(size_t)15;
-}
-
-__device__ __forceinline__ DecSmem dec_carve(char* base, int n) {
-  const int W = (n + 31) / 32;
-  DecSmem s;
-  char* p = base;
-  s.mv = (int64_t*)p; p += (size_t)n * 8;
-  s.am = (int64_t*)p; p += (size_t)n * 8;
-  s.R = (int64_t*)p; p += (size_t)(n + 1) * 8;
-  s.C = (int64_t*)p; p += (size_t)(n + 1) * 8;
-  s.sup = (uint32_t*)p; p += (size_t)n * W * 4;
-  s.seen = (uint32_t*)p; p += W * 4;
-  s.rm = (int16_t*)p; p += n * 2;
-  s.cm = (int16_t*)p; p += n * 2;
-  s.snap = (int16_t*)p; p += n * 2;
-  s.su = (int16_t*)p; p += n * 2;
-  s.sv = (int16_t*)p; p += n * 2;
-  s.freed = (int16_t*)p;
-  return s;
-}
-
-// augment(u, seen) of birkhoff.py:172-180 with a fresh `seen`, as an explicit
-// stack.  Columns are scanned in index order via first-set-bit over
-// support & ~seen, which visits exactly the v the reference's
-// `for v in range(n): if work[u][v] > 0 and not seen[v]` visits.
-__device__ bool augment_lane(const DecSmem& s, const int n, const int W,
-                             const int root) {
-  for (int w = 0; w < W; ++w) s.seen[w] = 0u;
-  int sp = 0;
-  s.su[0] = (int16_t)root;
-  int cur = 0;
-  for (;;) {
-    const int u = s.su[sp];
-    const uint32_t* su = s.sup + u * W;
-    int v = -1;
-    for (int w = cur >> 5; w < W; ++w) {
-      uint32_t bits = su[w] & ~s.seen[w];
-      if (w == (cur >> 5)) bits &= 0xffffffffu << (cur & 31);
-      if (bits) { v = (w << 5) + __ffs(bits) - 1; break; }
-    }
-    if (v < 0) {
-      if (sp == 0) return false;
-      --sp;
-      cur = s.sv[sp] + 1;
-      continue;
-    }
-    s.seen[v >> 5] |= 1u << (v & 31);
-    s.sv[sp] = (int16_t)v;
-    const int c = s.cm[v];
-    if (c < 0) {
-      for (int k = sp; k >= 0; --k) {
-        s.cm[s.sv[k]] = s.su[k];
-        s.rm[s.su[k]] = s.sv[k];
-      }
-      return true;
-    }
-    ++sp;
-    s.su[sp] = (int16_t)c;
-    cur = 0;
-  }
-}
-
 __device__ __forceinline__ int64_t warp_min_i64(int64_t v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -300,64 +250,240 @@ __device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
   return v;
 }
 
-struct DecWs {
-  int64_t* work;
-  int64_t* auxl;
-  uint64_t* key_w;
-  uint32_t* key_t;
-};
-
+// Per-matrix workspace: work matrix n*n int64, then sort keys (K x u64,
+// K x u32) for the kept stages.
 __host__ __device__ __forceinline__ size_t dec_ws_bytes_per_matrix(int n) {
   const size_t K = (size_t)stage_cap(n);
-  size_t b = 2 * (size_t)n * n * 8 + K * 8 + K * 4;
+  size_t b = (size_t)n * n * 8 + K * 8 + K * 4;
   return (b + 255) & ~(size_t)255;
 }
 
-__device__ __forceinline__ DecWs dec_ws(void* ws, int b, int n) {
-  char* p = (char*)ws + (size_t)b * dec_ws_bytes_per_matrix(n);
-  const size_t K = (size_t)stage_cap(n);
-  DecWs w;
-  w.work = (int64_t*)p; p += (size_t)n * n * 8;
-  w.auxl = (int64_t*)p; p += (size_t)n * n * 8;
-  w.key_w = (uint64_t*)p; p += K * 8;
-  w.key_t = (uint32_t*)p;
-  return w;
+// ---------------------------------------------------------------------------
+// Decomposition: one warp per matrix (birkhoff.py:75-252).
+//
+// State split:
+//   shared  sup[u]   support bitset of row u (work[u][v] > 0), NWP words
+//           supc[v]  copy of sup[cm[v]]: support of the row matched to v, so
+//                    one DFS step is a single 16-B shared load
+//           cm[v]    col_match; newcol[u] row's column after re-augmentation
+//           pick[k]  DFS stack: column chosen at depth k
+//   regs    lane owns rows u = r*32 + lane (r < NW): matched column, work
+//           value of its matched cell, and the off-diagonal demand there
+//   global  work[u][v] (embedded matrix, written back when a row leaves a
+//           non-zero cell) -- only touched when a row's match changes.
+// strip_auxiliary (birkhoff.py:225-252) is applied inline with the closed
+// form charged = min(w, max(0, work_before - off)): a cell's auxiliary bytes
+// are paid first, so aux_left = max(0, aux - peeled) = max(0, work - off).
+
+template <int NW>
+struct DecSh {
+  static constexpr int NQ = (NW + 1) / 2;   // u64 words per support row
+  static constexpr int NWP = 2 * NQ;        // u32 words per support row
+  uint32_t* sup;   // [n][NWP]
+  uint32_t* supc;  // [n][NWP]
+  int64_t* R;      // [n+1]
+  int64_t* C;      // [n+1]
+  int16_t* cm;     // [n]
+  int16_t* newcol; // [n]
+  int16_t* pick;   // [n]
+  int16_t* freed;  // [n]
+  uint32_t* chg;   // [NWP] rows whose match changed
+  uint32_t* freeb; // [NWP] free columns (cm < 0)
+};
+
+template <int NW>
+__host__ __device__ __forceinline__ size_t dec_smem_bytes_t(int n) {
+  constexpr int NWP = 2 * ((NW + 1) / 2);
+  size_t b = 2 * (size_t)n * NWP * 4;      // sup, supc
+  b += 2 * (size_t)(n + 1) * 8;            // R, C
+  b += 4 * (size_t)n * 2;                  // cm newcol pick freed
+  b += 2 * NWP * 4;                        // chg, freeb
+  return (b + 15) & ~(size_t)15;
 }
 
-// mode FAST_DEC_SERVER: S is a server matrix (diagonal ignored), embed first.
-// mode FAST_DEC_DOUBLY_STOCHASTIC: S is decomposed as-is, aux = 0.
-// check_total: synthesize path; S holds saturated tile totals and the status
-// word already carries the balance kernel's verdict.
+template <int NW>
+__device__ __forceinline__ DecSh<NW> dec_carve_t(char* p, int n) {
+  constexpr int NWP = DecSh<NW>::NWP;
+  DecSh<NW> s;
+  s.sup = (uint32_t*)p; p += (size_t)n * NWP * 4;
+  s.supc = (uint32_t*)p; p += (size_t)n * NWP * 4;
+  s.R = (int64_t*)p; p += (size_t)(n + 1) * 8;
+  s.C = (int64_t*)p; p += (size_t)(n + 1) * 8;
+  s.chg = (uint32_t*)p; p += NWP * 4;
+  s.freeb = (uint32_t*)p; p += NWP * 4;
+  s.cm = (int16_t*)p; p += n * 2;
+  s.newcol = (int16_t*)p; p += n * 2;
+  s.pick = (int16_t*)p; p += n * 2;
+  s.freed = (int16_t*)p;
+  return s;
+}
+
+template <int NQ>
+__device__ __forceinline__ void load_row(const uint32_t* src, uint64_t (&row)[NQ]) {
+  if constexpr (NQ == 2) {
+    const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(src);
+    row[0] = x.x;
+    row[1] = x.y;
+  } else {
+    row[0] = *reinterpret_cast<const uint64_t*>(src);
+  }
+}
+
+// Kuhn augment(root) with a fresh `seen` (birkhoff.py:172-180).
+// The reference scans v = 0..n-1 and descends into the first column with
+// work[u][v] > 0 that is not seen.  When a frame resumes after a failed
+// child, every support column left of the failed one is already seen, so
+// "first set bit of support & ~seen" is exactly the reference's next v; no
+// resume cursor is needed.  All 32 lanes run the search redundantly on
+// identical (broadcast) data, so the warp never diverges and the loop has no
+// reconvergence overhead.  Returns the depth of the successful path
+// (pick[k] = column taken at depth k, pick[depth] free) or -1.
+template <int NW>
+__device__ __forceinline__ int first_unseen(const uint32_t (&row)[2 * DecSh<NW>::NQ],
+                                            const uint32_t (&seen)[2 * DecSh<NW>::NQ]) {
+  constexpr int NWP = 2 * DecSh<NW>::NQ;
+  int best = 0x7fff;
+#pragma unroll
+  for (int w = 0; w < NWP; ++w) {
+    const uint32_t c = row[w] & ~seen[w];
+    const int f = c ? (w * 32 + __ffs(c) - 1) : 0x7fff;
+    best = f < best ? f : best;
+  }
+  return best;
+}
+
+template <int NW>
+__device__ __forceinline__ void load_row32(const uint32_t* src, uint32_t (&row)[2 * DecSh<NW>::NQ]) {
+  if constexpr (DecSh<NW>::NQ == 2) {
+    const uint4 x = *reinterpret_cast<const uint4*>(src);
+    row[0] = x.x; row[1] = x.y; row[2] = x.z; row[3] = x.w;
+  } else {
+    const uint2 x = *reinterpret_cast<const uint2*>(src);
+    row[0] = x.x; row[1] = x.y;
+  }
+}
+
+template <int NW>
+__device__ int dfs_search(const DecSh<NW>& s, const int root,
+                          const uint32_t (&freew)[2 * DecSh<NW>::NQ]) {
+  constexpr int NQ = DecSh<NW>::NQ;
+  constexpr int NWP = DecSh<NW>::NWP;
+  uint64_t freeq[NQ], seen[NQ], row[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    freeq[q] = (uint64_t)freew[2 * q] | ((uint64_t)freew[2 * q + 1] << 32);
+    seen[q] = 0ull;
+  }
+  load_row<NQ>(s.sup + root * NWP, row);
+  int sp = 0;
+  for (;;) {
+    const uint64_t c0 = row[0] & ~seen[0];
+    int v;
+    if constexpr (NQ == 2) {
+      const uint64_t c1 = row[1] & ~seen[1];
+      v = c0 ? __ffsll(c0) - 1 : (c1 ? 63 + __ffsll(c1) : -1);
+    } else {
+      v = c0 ? __ffsll(c0) - 1 : -1;
+    }
+    if (v < 0) {
+      if (sp == 0) return -1;
+      --sp;
+      load_row<NQ>(sp == 0 ? s.sup + root * NWP : s.supc + s.pick[sp - 1] * NWP, row);
+      continue;
+    }
+    const uint64_t bit = 1ull << (v & 63);
+    bool is_free;
+    if constexpr (NQ == 2) {
+      const bool hi = v >= 64;
+      seen[0] |= hi ? 0ull : bit;
+      seen[1] |= hi ? bit : 0ull;
+      is_free = ((hi ? freeq[1] : freeq[0]) & bit) != 0ull;
+    } else {
+      seen[0] |= bit;
+      is_free = (freeq[0] & bit) != 0ull;
+    }
+    s.pick[sp] = (int16_t)v;
+    if (is_free) return sp;
+    ++sp;
+    load_row<NQ>(s.supc + v * NWP, row);
+  }
+}
+
+// Lane 0 searches, the result is broadcast (the other lanes wait).
+template <int NW>
+__device__ __forceinline__ int dfs_warp(const DecSh<NW>& s, const int root,
+                                        const uint32_t (&freew)[2 * DecSh<NW>::NQ]) {
+#if FAST_DFS_ALL_LANES
+  return dfs_search<NW>(s, root, freew);
+#else
+  int depth = 0;
+  if ((threadIdx.x & 31) == 0) depth = dfs_search<NW>(s, root, freew);
+  return __shfl_sync(0xffffffffu, depth, 0);
+#endif
+}
+
+// Apply an augmenting path (warp-wide): cm[pick[k]] = row_k where row_0 =
+// root and row_{k+1} = old cm[pick[k]]; record new columns, refresh supc.
+template <int NW>
+__device__ __forceinline__ void apply_path(const DecSh<NW>& s, const int root,
+                                           const int depth, const int lane) {
+  constexpr int NWP = DecSh<NW>::NWP;
+  __syncwarp();  // lane 0's pick[] writes visible to the warp
+  int rows[(FAST_MAX_SERVERS + 31) / 32];
+#pragma unroll
+  for (int j = 0; j < (FAST_MAX_SERVERS + 31) / 32; ++j) {
+    const int k = j * 32 + lane;
+    rows[j] = (k <= depth) ? (k == 0 ? root : s.cm[s.pick[k - 1]]) : -1;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < (FAST_MAX_SERVERS + 31) / 32; ++j) {
+    const int k = j * 32 + lane;
+    if (k <= depth) {
+      const int v = s.pick[k], r = rows[j];
+      s.cm[v] = (int16_t)r;
+      s.newcol[r] = (int16_t)v;
+#pragma unroll
+      for (int w = 0; w < NWP; ++w) s.supc[v * NWP + w] = s.sup[r * NWP + w];
+      atomicOr(&s.chg[r >> 5], 1u << (r & 31));
+    }
+  }
+  __syncwarp();
+}
+
+template <int NW>
 __global__ void __launch_bounds__(kDecWarps * 32)
     decompose_kernel(const int64_t* __restrict__ S_all, const int B,
                      const int n, const int mode, const int check_total,
                      fast_sched_bufs out) {
+  constexpr int NWP = DecSh<NW>::NWP;
   extern __shared__ __align__(16) char dsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x * kDecWarps + warp;
   if (b >= B) return;
-  const int W = (n + 31) / 32;
   const int K = stage_cap(n);
-  DecSmem s = dec_carve(dsm + warp * dec_smem_bytes(n), n);
-  DecWs ws = dec_ws(out.workspace, b, n);
+  DecSh<NW> s = dec_carve_t<NW>(dsm + warp * dec_smem_bytes_t<NW>(n), n);
+  int64_t* work = (int64_t*)((char*)out.workspace + (size_t)b * dec_ws_bytes_per_matrix(n));
+  uint64_t* key_w = (uint64_t*)(work + (size_t)n * n);
+  uint32_t* key_t = (uint32_t*)(key_w + K);
   const int64_t* S = S_all + (int64_t)b * n * n;
   int32_t* status = out.status + b;
   int64_t* aux_out = out.aux + (int64_t)b * n * n;
 
   int st = check_total ? *status : FAST_OK;
 
-  // ---- row/column sums of the off-diagonal demand --------------------
-  int64_t colsum[FAST_MAX_SERVERS / 32];
+  // ---- row/column sums of the off-diagonal demand ------------------------
+  int64_t colsum[NW];
   int64_t rowmax = 0, tot = 0, row0 = 0;
   bool neg = false, ds_bad = false;
 #pragma unroll
-  for (int w = 0; w < FAST_MAX_SERVERS / 32; ++w) colsum[w] = 0;
+  for (int w = 0; w < NW; ++w) colsum[w] = 0;
   for (int u = 0; u < n; ++u) {
     int64_t rs = 0;
 #pragma unroll
-    for (int w = 0; w < FAST_MAX_SERVERS / 32; ++w) {
+    for (int w = 0; w < NW; ++w) {
       const int v = w * 32 + lane;
-      if (w < W && v < n) {
+      if (v < n) {
         int64_t x = S[(int64_t)u * n + v];
         if (x < 0) neg = true;
         tot = sat_add(tot, x < 0 ? 0 : x);
@@ -370,13 +496,13 @@ __global__ void __launch_bounds__(kDecWarps * 32)
     if (u == 0) row0 = rs;
     if (mode == FAST_DEC_DOUBLY_STOCHASTIC && rs != row0) ds_bad = true;
     rowmax = rs > rowmax ? rs : rowmax;
-    if (lane == 0) s.R[u + 1] = rs;  // row sums, turned into a prefix below
+    if (lane == 0) s.R[u + 1] = rs;  // row sums; turned into a prefix below
   }
   int64_t colmax = 0;
 #pragma unroll
-  for (int w = 0; w < FAST_MAX_SERVERS / 32; ++w) {
+  for (int w = 0; w < NW; ++w) {
     const int v = w * 32 + lane;
-    if (w < W && v < n) {
+    if (v < n) {
       colmax = colsum[w] > colmax ? colsum[w] : colmax;
       if (mode == FAST_DEC_DOUBLY_STOCHASTIC && colsum[w] != row0) ds_bad = true;
     }
@@ -384,7 +510,6 @@ __global__ void __launch_bounds__(kDecWarps * 32)
   colmax = warp_max_i64(colmax);
   neg = __any_sync(0xffffffffu, neg);
   ds_bad = __any_sync(0xffffffffu, ds_bad);
-  // matrix total (saturating): lanes hold saturated partial sums
   int64_t all = 0;
   for (int l = 0; l < 32; ++l) all = sat_add(all, __shfl_sync(0xffffffffu, tot, l));
   if (st == FAST_OK) {
@@ -393,7 +518,6 @@ __global__ void __launch_bounds__(kDecWarps * 32)
   }
   const int64_t common =
       mode == FAST_DEC_DOUBLY_STOCHASTIC ? row0 : (rowmax > colmax ? rowmax : colmax);
-
   if (st != FAST_OK) {
     if (lane == 0) {
       *status = st;
@@ -404,11 +528,11 @@ __global__ void __launch_bounds__(kDecWarps * 32)
     return;
   }
 
-  // ---- embedding: northwest corner as interval overlap -----------------
+  // ---- embedding: northwest corner == interval overlap of deficit prefixes
 #pragma unroll
-  for (int w = 0; w < FAST_MAX_SERVERS / 32; ++w) {
+  for (int w = 0; w < NW; ++w) {
     const int v = w * 32 + lane;
-    if (w < W && v < n) s.C[v + 1] = common - colsum[w];
+    if (v < n) s.C[v + 1] = common - colsum[w];
   }
   __syncwarp();
   if (lane == 0) {
@@ -417,17 +541,22 @@ __global__ void __launch_bounds__(kDecWarps * 32)
     for (int u = 0; u < n; ++u) s.R[u + 1] = s.R[u] + (common - s.R[u + 1]);
     for (int v = 0; v < n; ++v) s.C[v + 1] += s.C[v];
   }
-  for (int u = lane; u < n; u += 32) { s.rm[u] = -1; s.cm[u] = -1; }
+  for (int u = lane; u < n; u += 32) s.cm[u] = -1;
+  if (lane < NWP) {
+    s.chg[lane] = 0u;
+    const int lo = lane * 32;
+    s.freeb[lane] = lo >= n ? 0u : (n - lo >= 32 ? 0xffffffffu : ((1u << (n - lo)) - 1u));
+  }
   __syncwarp();
   for (int u = 0; u < n; ++u) {
     const int64_t r0 = s.R[u], r1 = s.R[u + 1];
-    for (int w = 0; w < W; ++w) {
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
       const int v = w * 32 + lane;
       int64_t e = 0;
       if (v < n) {
-        const int64_t x = S[(int64_t)u * n + v];
+        int64_t off = S[(int64_t)u * n + v];
         int64_t a = 0;
-        int64_t off = x;
         if (mode == FAST_DEC_SERVER) {
           if (u == v) off = 0;
           const int64_t lo = r0 > s.C[v] ? r0 : s.C[v];
@@ -436,16 +565,15 @@ __global__ void __launch_bounds__(kDecWarps * 32)
         }
         e = off + a;
         aux_out[(int64_t)u * n + v] = a;
-        ws.work[(int64_t)u * n + v] = e;
-        ws.auxl[(int64_t)u * n + v] = a;
+        work[(int64_t)u * n + v] = e;
       }
       const uint32_t bits = __ballot_sync(0xffffffffu, e > 0);
-      if (lane == 0) s.sup[u * W + w] = bits;
+      if (lane == 0) s.sup[u * NWP + w] = bits;
     }
+    if (NWP > NW && lane == 0) s.sup[u * NWP + NWP - 1] = 0u;
   }
   if (lane == 0) out.common_sum[b] = common;
   __syncwarp();
-
   if (common == 0) {
     if (lane == 0) {
       out.n_raw[b] = 0;
@@ -456,24 +584,43 @@ __global__ void __launch_bounds__(kDecWarps * 32)
   }
 
   // ---- initial Kuhn matching (birkhoff.py:182-186) -----------------------
-  int ok = 1;
-  if (lane == 0) {
-    for (int u = 0; u < n && ok; ++u) ok = augment_lane(s, n, W, u);
+  uint32_t freew[NWP];
+#pragma unroll
+  for (int w = 0; w < NWP; ++w) freew[w] = s.freeb[w];
+  for (int u = 0; u < n; ++u) {
+    const int depth = dfs_warp<NW>(s, u, freew);
+    if (depth < 0) { st = FAST_EINVARIANT; break; }
+    apply_path<NW>(s, u, depth, lane);
+    const int vf = s.pick[depth];
+#pragma unroll
+    for (int w = 0; w < NWP; ++w)
+      if ((vf >> 5) == w) freew[w] &= ~(1u << (vf & 31));
   }
-  ok = __shfl_sync(0xffffffffu, ok, 0);
-  __syncwarp();
-  if (!ok) {
-    if (lane == 0) { *status = FAST_EINVARIANT; out.n_raw[b] = 0; out.n_stages[b] = 0; }
+  if (st != FAST_OK) {
+    if (lane == 0) { *status = st; out.n_raw[b] = 0; out.n_stages[b] = 0; }
     return;
   }
-  for (int u = lane; u < n; u += 32) {
-    const int v = s.rm[u];
-    s.mv[u] = ws.work[(int64_t)u * n + v];
-    s.am[u] = ws.auxl[(int64_t)u * n + v];
+  if (lane < NWP) s.freeb[lane] = 0u;  // perfect matching: no free column
+  // lane-owned row state
+  int rcol[NW];
+  int64_t mv[NW], offv[NW];
+#pragma unroll
+  for (int r = 0; r < NW; ++r) {
+    const int u = r * 32 + lane;
+    rcol[r] = -1;
+    mv[r] = INT64_MAX;
+    offv[r] = 0;
+    if (u < n) {
+      const int v = s.newcol[u];
+      rcol[r] = v;
+      mv[r] = work[(int64_t)u * n + v];
+      offv[r] = (mode == FAST_DEC_SERVER && u == v) ? 0 : S[(int64_t)u * n + v];
+    }
   }
+  if (lane < NWP) s.chg[lane] = 0u;
   __syncwarp();
 
-  // ---- peel loop (birkhoff.py:190-219) fused with strip (:225-252) -------
+  // ---- peel loop (birkhoff.py:190-219) fused with strip -----------------
   int64_t remaining = common;
   int k = 0, kept = 0;
   int64_t* wout = out.stage_weight + (int64_t)b * K;
@@ -482,92 +629,113 @@ __global__ void __launch_bounds__(kDecWarps * 32)
   while (remaining > 0) {
     if (k >= K) { st = FAST_EINVARIANT; break; }
     int64_t wl = INT64_MAX;
-    for (int u = lane; u < n; u += 32) wl = s.mv[u] < wl ? s.mv[u] : wl;
+#pragma unroll
+    for (int r = 0; r < NW; ++r) wl = mv[r] < wl ? mv[r] : wl;
     const int64_t weight = warp_min_i64(wl);
     if (weight <= 0) { st = FAST_EINVARIANT; break; }
     remaining -= weight;
-    int src0 = -1;
-    int nfreed = 0;
-    for (int base = 0; base < n; base += 32) {
-      const int u = base + lane;
+    int src0 = -1, nfreed = 0, dst0 = 0;
+#pragma unroll
+    for (int r = 0; r < NW; ++r) {
+      const int u = r * 32 + lane;
       bool real_pos = false, fr = false;
+      const int vsave = rcol[r];
       if (u < n) {
-        const int v = s.rm[u];
-        const int64_t mvu = s.mv[u] - weight;
-        const int64_t amu = s.am[u];
-        const int64_t charged = amu < weight ? amu : weight;
+        const int v = rcol[r];
+        const int64_t before = mv[r];
+        const int64_t spare = before - offv[r];
+        const int64_t charged = spare <= 0 ? 0 : (spare < weight ? spare : weight);
         const int64_t real = weight - charged;
-        s.mv[u] = mvu;
-        s.am[u] = amu - charged;
-        bout[(int64_t)k * n + u] = real;
+        mv[r] = before - weight;
+        __stcs(bout + (int64_t)k * n + u, real);
         pout[(int64_t)k * n + u] = (uint8_t)v;
         real_pos = real > 0;
-        if (mvu == 0) {
-          s.sup[u * W + (v >> 5)] &= ~(1u << (v & 31));
+        if (mv[r] == 0) {
+          s.sup[u * NWP + (v >> 5)] &= ~(1u << (v & 31));
           fr = remaining > 0;
         }
       }
       const uint32_t rb = __ballot_sync(0xffffffffu, real_pos);
-      if (src0 < 0 && rb) src0 = base + __ffs(rb) - 1;
+      if (src0 < 0 && rb) {
+        src0 = r * 32 + __ffs(rb) - 1;
+        dst0 = __shfl_sync(0xffffffffu, vsave, __ffs(rb) - 1);
+      }
       const uint32_t fb = __ballot_sync(0xffffffffu, fr);
-      if (fr) s.freed[nfreed + __popc(fb & ((1u << lane) - 1u))] = (int16_t)u;
+      if (fr) {
+        s.freed[nfreed + __popc(fb & ((1u << lane) - 1u))] = (int16_t)u;
+        s.cm[rcol[r]] = -1;  // unmatch (birkhoff.py:210-214)
+        atomicOr(&s.freeb[rcol[r] >> 5], 1u << (rcol[r] & 31));
+        rcol[r] = -1;
+      }
       nfreed += __popc(fb);
     }
     if (lane == 0) {
       wout[k] = weight;
       if (src0 >= 0) {
-        ws.key_w[kept] = (uint64_t)weight;
-        ws.key_t[kept] = ((uint32_t)src0 << 24) | ((uint32_t)s.rm[src0] << 16) |
-                         (uint32_t)k;
+        // dst of src0 = the column src0 was matched to in this stage
+        key_w[kept] = (uint64_t)weight;
+        key_t[kept] = ((uint32_t)src0 << 24) | ((uint32_t)dst0 << 16) | (uint32_t)k;
       }
     }
     if (src0 >= 0) ++kept;
     ++k;
     if (remaining == 0) break;
     __syncwarp();
-    // unmatch freed rows, remember every row's cell
-    for (int u = lane; u < n; u += 32) s.snap[u] = s.rm[u];
-    __syncwarp();
-    for (int f = lane; f < nfreed; f += 32) {
+    // re-augment freed rows in index order (birkhoff.py:215-219)
+#pragma unroll
+    for (int w = 0; w < NWP; ++w) freew[w] = s.freeb[w];
+    for (int f = 0; f < nfreed; ++f) {
       const int u = s.freed[f];
-      const int v = s.rm[u];
-      if (s.cm[v] == u) s.cm[v] = -1;
-      s.rm[u] = -1;
+      const int depth = dfs_warp<NW>(s, u, freew);
+      if (depth < 0) { st = FAST_EINVARIANT; break; }
+      apply_path<NW>(s, u, depth, lane);
+      const int vf = s.pick[depth];
+#pragma unroll
+      for (int w = 0; w < NWP; ++w)
+        if ((vf >> 5) == w) freew[w] &= ~(1u << (vf & 31));
     }
+    if (st != FAST_OK) break;
     __syncwarp();
-    if (lane == 0) {
-      for (int f = 0; f < nfreed && ok; ++f) {
-        const int u = s.freed[f];
-        if (s.rm[u] < 0) ok = augment_lane(s, n, W, u);
+    if (lane < NWP) {
+#pragma unroll
+      for (int w = 0; w < NWP; ++w)
+        if (lane == w) s.freeb[w] = freew[w];
+    }
+    // rows whose cell changed: write the old (non-zero) value back, fetch
+    // the new cell; all loads are issued before any is consumed.
+    uint32_t chg[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) chg[w] = s.chg[w];
+    __syncwarp();
+    if (lane < NWP) s.chg[lane] = 0u;
+    int64_t nv[NW], no[NW];
+    bool moved[NW];
+#pragma unroll
+    for (int r = 0; r < NW; ++r) {
+      const int u = r * 32 + lane;
+      moved[r] = u < n && ((chg[r] >> lane) & 1u);
+      if (moved[r]) {
+        const int nc = s.newcol[u];
+        if (rcol[r] >= 0) work[(int64_t)u * n + rcol[r]] = mv[r];
+        rcol[r] = nc;
+        nv[r] = work[(int64_t)u * n + nc];
+        no[r] = S[(int64_t)u * n + nc];
       }
     }
-    ok = __shfl_sync(0xffffffffu, ok, 0);
-    __syncwarp();
-    if (!ok) { st = FAST_EINVARIANT; break; }
-    // rows whose cell changed: write the old cell back, fetch the new one
-    for (int u = lane; u < n; u += 32) {
-      const int old = s.snap[u], now = s.rm[u];
-      if (old != now) {
-        ws.work[(int64_t)u * n + old] = s.mv[u];
-        ws.auxl[(int64_t)u * n + old] = s.am[u];
-        s.mv[u] = ws.work[(int64_t)u * n + now];
-        s.am[u] = ws.auxl[(int64_t)u * n + now];
+#pragma unroll
+    for (int r = 0; r < NW; ++r) {
+      if (moved[r]) {
+        mv[r] = nv[r];
+        offv[r] = (mode == FAST_DEC_SERVER && r * 32 + lane == rcol[r]) ? 0 : no[r];
       }
     }
     __syncwarp();
   }
 
-  // ---- final invariants (birkhoff.py:216-221, :250-251, :273-277) --------
+  // ---- final invariants (birkhoff.py:216-221, :273-277): every cell peeled
   if (st == FAST_OK) {
-    for (int u = lane; u < n; u += 32) {
-      const int v = s.rm[u];
-      ws.work[(int64_t)u * n + v] = s.mv[u];
-      ws.auxl[(int64_t)u * n + v] = s.am[u];
-    }
-    __syncwarp();
-    bool left = false;
-    for (int c = lane; c < n * n; c += 32)
-      left |= (ws.work[c] != 0) | (ws.auxl[c] != 0);
+    bool left = remaining != 0;
+    for (int c = lane; c < n * NWP; c += 32) left |= s.sup[c] != 0u;
     if (__any_sync(0xffffffffu, left)) st = FAST_EINVARIANT;
   }
   if (lane == 0) {
@@ -593,11 +761,14 @@ __global__ void __launch_bounds__(1024)
   if (kept <= 0) return;
   int Q = 1;
   while (Q < kept) Q <<= 1;
-  DecWs ws = dec_ws(out.workspace, b, n);
+  const int64_t* work =
+      (const int64_t*)((const char*)out.workspace + (size_t)b * dec_ws_bytes_per_matrix(n));
+  const uint64_t* key_w = (const uint64_t*)(work + (size_t)n * n);
+  const uint32_t* key_t = (const uint32_t*)(key_w + K);
   for (int i = threadIdx.x; i < Q; i += blockDim.x) {
     if (i < kept) {
-      kw[i] = ws.key_w[i];
-      kt[i] = ws.key_t[i];
+      kw[i] = key_w[i];
+      kt[i] = key_t[i];
     } else {
       kw[i] = ~0ull;
       kt[i] = ~0u;
@@ -637,10 +808,12 @@ int check(cudaError_t e) { return e == cudaSuccess ? FAST_OK : FAST_ECUDA; }
 int launch_balance(const int64_t* D, int B, int n, int m,
                    const fast_sched_bufs* out, cudaStream_t s) {
   const size_t tile_bytes = (size_t)(m * m + 1) * 8;
-  int J = (int)((96 * 1024) / tile_bytes);
-  if (J > kBalThreads) J = kBalThreads;
+  // ~32 KiB strips: several CTAs per SM overlap the per-tile sequential
+  // balancing of one CTA with the HBM traffic of the others.
+  int J = (int)((32 * 1024) / tile_bytes);
+  if (J > 64) J = 64;
   if (J > n) J = n;
-  if (J < 1) return FAST_EVALIDATION;
+  if (J < 1) J = 1;  // m >= 45: one 16+ KiB tile per CTA
   const size_t smem = (size_t)J * tile_bytes;
   dim3 grid(n, (n + J - 1) / J, B);
   cudaError_t e;
@@ -669,17 +842,31 @@ int launch_balance(const int64_t* D, int B, int n, int m,
   return check(cudaGetLastError());
 }
 
-int launch_decompose(const int64_t* S, int B, int n, int mode, int check_total,
-                     const fast_sched_bufs* out, cudaStream_t s,
-                     cudaEvent_t after_decompose = nullptr) {
-  const size_t smem = dec_smem_bytes(n) * kDecWarps;
-  if (cudaFuncSetAttribute(decompose_kernel,
+template <int NW>
+int launch_decompose_t(const int64_t* S, int B, int n, int mode, int check_total,
+                       const fast_sched_bufs* out, cudaStream_t s) {
+  const size_t smem = dec_smem_bytes_t<NW>(n) * kDecWarps;
+  if (cudaFuncSetAttribute(decompose_kernel<NW>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)
     return FAST_ECUDA;
   const int grid = (B + kDecWarps - 1) / kDecWarps;
-  decompose_kernel<<<grid, kDecWarps * 32, smem, s>>>(S, B, n, mode,
-                                                      check_total, *out);
+  decompose_kernel<NW><<<grid, kDecWarps * 32, smem, s>>>(S, B, n, mode,
+                                                          check_total, *out);
+  return FAST_OK;
+}
+
+int launch_decompose(const int64_t* S, int B, int n, int mode, int check_total,
+                     const fast_sched_bufs* out, cudaStream_t s,
+                     cudaEvent_t after_decompose = nullptr) {
+  int rc;
+  switch ((n + 31) / 32) {
+    case 1: rc = launch_decompose_t<1>(S, B, n, mode, check_total, out, s); break;
+    case 2: rc = launch_decompose_t<2>(S, B, n, mode, check_total, out, s); break;
+    case 3: rc = launch_decompose_t<3>(S, B, n, mode, check_total, out, s); break;
+    default: rc = launch_decompose_t<4>(S, B, n, mode, check_total, out, s); break;
+  }
+  if (rc != FAST_OK) return rc;
   if (cudaGetLastError() != cudaSuccess) return FAST_ECUDA;
   if (after_decompose && cudaEventRecord(after_decompose, s) != cudaSuccess)
     return FAST_ECUDA;

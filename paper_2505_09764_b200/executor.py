@@ -1,0 +1,348 @@
+"""FAST alltoallv execution over NVSwitch -- the executor the reference only
+models (tiersched.simulate_fast, simulate.py:107-193).
+
+    comm = FastComm(Topology(2, 4))            # one process per GPU (torchrun)
+    recv = comm.alltoallv(send, send_counts)  # device bytes, stream-ordered
+    all_to_all_fast(out, inp, out_splits, in_splits, comm=comm)
+
+Per call, everything stays on the device (no host synchronisation):
+  1. fast_gather_demand  P2P all-gather of the per-rank byte counts -> D
+  2. fast_synth_batch    the FAST schedule for D (identical on every rank)
+  3. fast_plan_compile   Appendix-A byte placement -> phase-ordered copy ops
+  4. fast_exec           one persistent P2P kernel per rank over NVSwitch
+The GPUs are split into virtual servers (n x m = world, e.g. 2x4 or 4x2):
+phase 1 (balance) and the one-to-one stages both run over NVLink.
+
+``GroupComm`` runs the same kernels for all ranks on ONE device (a
+cooperative launch), used by the single-GPU parity tests.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .model import Topology, ValidationError, validate_topology
+from .synth import SynthBuffers, _device, _stream_handle
+
+OP_DTYPE = np.dtype([("src_off", "<i8"), ("dst_off", "<i8"), ("len", "<i8"),
+                     ("exec_rank", "<i2"), ("dst_rank", "<i2"), ("src_buf", "u1"),
+                     ("dst_buf", "u1"), ("phase", "u1"), ("stage", "u1")])
+PH_BALANCE, PH_DIRECT, PH_FROM_STAGING, PH_REDIST = 0, 1, 2, 3
+BUF_SEND, BUF_RECV, BUF_STAGING = 0, 1, 2
+TIMELINE_STRIDE = 8 + 256
+DEFAULT_BLOCKS = 32
+DEFAULT_CHUNK = 256 * 1024
+
+
+@dataclass(frozen=True)
+class Timeline:
+    """Per-phase breakdown, shaped like tiersched's (simulate.py:38-55), but
+    MEASURED on the device (seconds).  scale_out[k] is the time from the
+    barrier until stage k's bytes had all arrived at this rank's staging
+    (0 where this rank proxies nothing in stage k)."""
+
+    t_balance: float
+    t_intra_a2a: float
+    scale_out: tuple[float, ...]
+    redistribution: tuple[float, ...]
+    total: float
+
+    def to_json_dict(self) -> dict:
+        return {"t_balance": self.t_balance, "t_intra_a2a": self.t_intra_a2a,
+                "scale_out": list(self.scale_out), "redistribution": list(self.redistribution),
+                "total": self.total}
+
+
+class _CudaBytes:
+    """Zero-copy torch view of raw device memory (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+def bytes_view(ptr: int, nbytes: int, device) -> torch.Tensor:
+    return torch.as_tensor(_CudaBytes(ptr, nbytes), device=device)
+
+
+class PlanBuffers:
+    """Device buffers of one compiled plan (fast_plan)."""
+
+    def __init__(self, n: int, m: int, device):
+        lib = _lib.load()
+        G = n * m
+        self.capacity = int(lib.fast_plan_op_capacity(n, m))
+        self.ops = torch.empty(self.capacity * OP_DTYPE.itemsize, dtype=torch.uint8, device=device)
+        self.n_ops = torch.zeros(1, dtype=torch.int32, device=device)
+        self.staging_used = torch.zeros(G, dtype=torch.int64, device=device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=device)
+        self.ws = torch.empty(int(lib.fast_plan_workspace_bytes(n, m)) + 16, dtype=torch.uint8,
+                              device=device)
+        self.struct = _lib.FastPlan(self.ops.data_ptr(), self.n_ops.data_ptr(),
+                                    self.staging_used.data_ptr(), self.status.data_ptr(),
+                                    self.ws.data_ptr(), self.capacity)
+
+    def host_ops(self) -> np.ndarray:
+        k = int(self.n_ops.item())
+        return self.ops[: k * OP_DTYPE.itemsize].cpu().numpy().view(OP_DTYPE)
+
+
+def plan_compile_host(D: np.ndarray, n: int, m: int, order: np.ndarray, perm: np.ndarray,
+                      sbytes: np.ndarray, recv_cap: int, staging_cap: int):
+    """Host build of the plan logic (validation / inspection only)."""
+    lib = _lib.load()
+    D = np.ascontiguousarray(D, dtype=np.int64)
+    K = n * n - 2 * n + 2
+    perm_k = np.zeros((K, n), np.uint8)
+    perm_k[: perm.shape[0]] = perm
+    sb_k = np.zeros((K, n), np.int64)
+    sb_k[: sbytes.shape[0]] = sbytes
+    order = np.ascontiguousarray(order, dtype=np.int32)
+    cap = int(lib.fast_plan_op_capacity(n, m))
+    ops = np.zeros(cap, OP_DTYPE)
+    n_ops = np.zeros(1, np.int32)
+    used = np.zeros(n * m, np.int64)
+    ws = np.zeros(int(lib.fast_plan_workspace_bytes(n, m)) + 16, np.uint8)
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    st = lib.fast_plan_compile_host(p(D), n, m, int(order.shape[0]), p(order), p(perm_k),
+                                    p(sb_k), int(recv_cap), int(staging_cap), p(ops), cap,
+                                    p(n_ops), p(used), p(ws))
+    return ops[: int(n_ops[0])].copy(), used, int(st)
+
+
+def _timeline_from(stamps: np.ndarray, ops: np.ndarray | None, rank: int) -> Timeline:
+    t0 = stamps[1]
+    sec = lambda x: max(0.0, (int(x) - int(t0)) * 1e-9) if x else 0.0  # noqa: E731
+    n_st = 0
+    if ops is not None and len(ops):
+        n_st = int(ops["stage"].max()) + 1
+    so = tuple(sec(stamps[8 + k]) for k in range(n_st))
+    return Timeline(t_balance=sec(stamps[2]), t_intra_a2a=0.0, scale_out=so,
+                    redistribution=tuple(0.0 for _ in so), total=sec(stamps[4]))
+
+
+class FastComm:
+    """One rank of the FAST executor (torch.distributed process group)."""
+
+    def __init__(self, topology: Topology, recv_bytes: int, staging_bytes: int | None = None,
+                 group=None, blocks: int = DEFAULT_BLOCKS, chunk_bytes: int = DEFAULT_CHUNK):
+        import torch.distributed as dist
+
+        validate_topology(topology)
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if topology.gpu_count != self.world:
+            raise ValidationError(f"topology {topology.n_servers}x{topology.gpus_per_server} "
+                                  f"needs {topology.gpu_count} ranks, group has {self.world}")
+        self.topology = topology
+        self.device = _device()
+        self.recv_bytes = int(recv_bytes)
+        self.staging_bytes = int(staging_bytes if staging_bytes is not None else recv_bytes)
+        self.blocks, self.chunk = blocks, chunk_bytes
+        lib = _lib.load()
+        ptr = ctypes.c_void_p()
+        _lib.check_rc(lib.fast_comm_create(self.rank, self.world, 0, self.recv_bytes,
+                                           self.staging_bytes, ctypes.byref(ptr)),
+                      "fast_comm_create")
+        self._ptr = ptr
+        h = (ctypes.c_uint8 * 64)()
+        _lib.check_rc(lib.fast_comm_ipc_handle(ptr, h), "fast_comm_ipc_handle")
+        handles: list = [None] * self.world
+        dist.all_gather_object(handles, bytes(h), group=group)
+        blob = b"".join(handles)
+        _lib.check_rc(lib.fast_comm_open_peers(ptr, blob), "fast_comm_open_peers")
+        dist.barrier(group=group)
+        n, m = topology.n_servers, topology.gpus_per_server
+        self.sched = SynthBuffers(1, n, m, self.device)
+        self.plan = PlanBuffers(n, m, self.device)
+        self.timeline = torch.zeros(TIMELINE_STRIDE, dtype=torch.int64, device=self.device)
+        self.epoch = 0
+        self.recv = bytes_view(lib.fast_comm_recv_ptr(ptr), self.recv_bytes, self.device)
+
+    def close(self) -> None:
+        if getattr(self, "_ptr", None):
+            _lib.load().fast_comm_destroy(self._ptr)
+            self._ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def demand(self) -> torch.Tensor:
+        """The gathered G x G demand matrix of the last call (device)."""
+        lib = _lib.load()
+        ptr = lib.fast_comm_demand_ptr(self._ptr, self.epoch)
+        G = self.world
+        return bytes_view(ptr, G * G * 8, self.device).view(torch.int64).view(G, G)
+
+    def alltoallv(self, send: torch.Tensor, send_counts: torch.Tensor,
+                  stream: torch.cuda.Stream | None = None, record_timeline: bool = False
+                  ) -> torch.Tensor:
+        """FAST alltoallv of `send` (uint8, device) split by send_counts
+        (int64[world] device, bytes per destination, own entry ignored).
+        Returns the recv region (source-major segments, self excluded)."""
+        lib = _lib.load()
+        if send.dtype != torch.uint8 or not send.is_cuda:
+            raise ValidationError("send must be a cuda uint8 tensor")
+        n, m = self.topology.n_servers, self.topology.gpus_per_server
+        row = send_counts.to(device=self.device, dtype=torch.int64).clone()
+        row[self.rank] = 0
+        self._row = row  # keep alive until the stream consumes it
+        self.epoch += 1
+        sh = _stream_handle(stream)
+        _lib.check_rc(lib.fast_gather_demand(self._ptr, ctypes.c_void_p(row.data_ptr()),
+                                             self.epoch, sh), "fast_gather_demand")
+        dptr = lib.fast_comm_demand_ptr(self._ptr, self.epoch)
+        _lib.check_rc(lib.fast_synth_batch(ctypes.c_void_p(dptr), 1, n, m,
+                                           ctypes.byref(self.sched.struct), sh), "fast_synth_batch")
+        _lib.check_rc(lib.fast_plan_compile(ctypes.c_void_p(dptr), n, m,
+                                            ctypes.byref(self.sched.struct), self.recv_bytes,
+                                            self.staging_bytes, ctypes.byref(self.plan.struct), sh),
+                      "fast_plan_compile")
+        tl = ctypes.c_void_p(self.timeline.data_ptr()) if record_timeline else None
+        _lib.check_rc(lib.fast_exec(self._ptr, ctypes.byref(self.plan.struct),
+                                    ctypes.c_void_p(send.data_ptr()), self.epoch, self.blocks,
+                                    self.chunk, tl, sh), "fast_exec")
+        return self.recv
+
+    def check(self) -> None:
+        """Raise if the last call's device status reports a failure (syncs)."""
+        st = ctypes.c_int32()
+        _lib.check_rc(_lib.load().fast_comm_status(self._ptr, ctypes.byref(st)), "status")
+        plan_st = int(self.plan.status.item())
+        if plan_st != 0:
+            _lib.check_rc(plan_st, "fast_plan_compile")
+        if st.value != 0:
+            _lib.check_rc(3, "fast_exec (timeout / protocol)")
+
+    def measured_timeline(self) -> Timeline:
+        return _timeline_from(self.timeline.cpu().numpy(), self.plan.host_ops(), self.rank)
+
+
+def all_to_all_fast(output: torch.Tensor, input: torch.Tensor,
+                    output_split_sizes: list[int] | None = None,
+                    input_split_sizes: list[int] | None = None,
+                    comm: FastComm | None = None) -> torch.Tensor:
+    """Drop-in for torch.distributed.all_to_all_single on the
+    FAST path.  Splits are along dim 0 in rows; the self segment is a local
+    copy, everything else goes through comm.alltoallv."""
+    if comm is None:
+        raise ValidationError("all_to_all_fast needs a FastComm")
+    W = comm.world
+    rows_in, rows_out = input.shape[0], output.shape[0]
+    row_bytes = input[0].numel() * input.element_size() if rows_in else 0
+    if input_split_sizes is None:
+        input_split_sizes = [rows_in // W] * W
+    if output_split_sizes is None:
+        output_split_sizes = [rows_out // W] * W
+    inb = input.contiguous().view(torch.uint8).reshape(-1)
+    counts = torch.tensor([s * row_bytes for s in input_split_sizes], dtype=torch.int64,
+                          device=input.device)
+    recv = comm.alltoallv(inb, counts)
+    outb = output.view(torch.uint8).reshape(-1)
+    r = comm.rank
+    self_in = sum(input_split_sizes[:r]) * row_bytes
+    self_out = sum(output_split_sizes[:r]) * row_bytes
+    nself = input_split_sizes[r] * row_bytes
+    before = self_out
+    after = sum(output_split_sizes[r + 1:]) * row_bytes
+    if before:
+        outb[:before].copy_(recv[:before])
+    if nself:
+        outb[self_out:self_out + nself].copy_(inb[self_in:self_in + nself])
+    if after:
+        outb[self_out + nself:self_out + nself + after].copy_(recv[before:before + after])
+    return output
+
+
+class GroupComm:
+    """All `world` ranks on ONE device: same plan + exec kernels, launched as
+    one cooperative kernel (tests, single-GPU benchmarks of the protocol)."""
+
+    def __init__(self, topology: Topology, recv_bytes: int, staging_bytes: int | None = None,
+                 blocks: int = 8, chunk_bytes: int = DEFAULT_CHUNK):
+        validate_topology(topology)
+        self.topology = topology
+        self.world = topology.gpu_count
+        self.device = _device()
+        self.recv_bytes = int(recv_bytes)
+        self.staging_bytes = int(staging_bytes if staging_bytes is not None else recv_bytes)
+        self.blocks, self.chunk = blocks, chunk_bytes
+        lib = _lib.load()
+        arr = (ctypes.c_void_p * self.world)()
+        _lib.check_rc(lib.fast_comm_create_group(self.world, self.recv_bytes, self.staging_bytes,
+                                                 arr), "fast_comm_create_group")
+        self._ptrs = arr
+        n, m = topology.n_servers, topology.gpu_count // topology.n_servers
+        self.sched = SynthBuffers(1, n, m, self.device)
+        self.plan = PlanBuffers(n, m, self.device)
+        self.timeline = torch.zeros(self.world * TIMELINE_STRIDE, dtype=torch.int64,
+                                    device=self.device)
+        self.epoch = 0
+        self.recvs = [bytes_view(lib.fast_comm_recv_ptr(ctypes.c_void_p(p)), self.recv_bytes,
+                                 self.device) for p in arr]
+
+    def close(self) -> None:
+        if getattr(self, "_ptrs", None) is not None:
+            lib = _lib.load()
+            for p in self._ptrs:
+                lib.fast_comm_destroy(ctypes.c_void_p(p))
+            self._ptrs = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def alltoallv(self, sends: list[torch.Tensor], D: torch.Tensor,
+                  stream: torch.cuda.Stream | None = None) -> list[torch.Tensor]:
+        lib = _lib.load()
+        n, m = self.topology.n_servers, self.topology.gpus_per_server
+        if D.dtype != torch.int64 or tuple(D.shape) != (self.world, self.world):
+            raise ValidationError("D must be int64 [world, world]")
+        self._D = D.to(self.device).contiguous()
+        self.epoch += 1
+        sh = _stream_handle(stream)
+        dp = ctypes.c_void_p(self._D.data_ptr())
+        _lib.check_rc(lib.fast_synth_batch(dp, 1, n, m, ctypes.byref(self.sched.struct), sh),
+                      "fast_synth_batch")
+        _lib.check_rc(lib.fast_plan_compile(dp, n, m, ctypes.byref(self.sched.struct),
+                                            self.recv_bytes, self.staging_bytes,
+                                            ctypes.byref(self.plan.struct), sh),
+                      "fast_plan_compile")
+        sp = (ctypes.c_void_p * self.world)(*[s.data_ptr() for s in sends])
+        _lib.check_rc(lib.fast_exec_group(self._ptrs, self.world, ctypes.byref(self.plan.struct),
+                                          sp, self.epoch, self.blocks, self.chunk,
+                                          ctypes.c_void_p(self.timeline.data_ptr()), sh),
+                      "fast_exec_group")
+        return self.recvs
+
+    def check(self) -> None:
+        lib = _lib.load()
+        plan_st = int(self.plan.status.item())
+        if plan_st != 0:
+            _lib.check_rc(plan_st, "fast_plan_compile")
+        for p in self._ptrs:
+            st = ctypes.c_int32()
+            _lib.check_rc(lib.fast_comm_status(ctypes.c_void_p(p), ctypes.byref(st)), "status")
+            if st.value != 0:
+                _lib.check_rc(3, "fast_exec_group (timeout / protocol)")
+
+
+def execute_fast(comm: FastComm, send: torch.Tensor, send_counts: torch.Tensor) -> torch.Tensor:
+    """Alias of comm.alltoallv (the executor behind simulate_fast's API)."""
+    return comm.alltoallv(send, send_counts)
+
+
+def simulate_fast(*args, **kwargs):  # pragma: no cover - API pointer
+    raise NotImplementedError(
+        "the analytical cost model is out of scope on B200; use FastComm.alltoallv + "
+        "measured_timeline() (the executor this path replaces)")
