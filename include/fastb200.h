@@ -146,8 +146,11 @@ size_t fast_plan_workspace_bytes(int n, int m);
 int64_t fast_plan_op_capacity(int n, int m);
 
 /* Plan compile on the device (one-thread kernel, stream-ordered): D [G][G]
- * and the packed schedule of matrix 0 of `sched` -> phase-ordered ops. */
-int fast_plan_compile(const int64_t *D, int n, int m,
+ * (zero diagonal) and the packed schedule of matrix 0 of `sched` ->
+ * phase-ordered ops.  send_self (device int64[G] or NULL): bytes of each
+ * rank's own segment, kept in place inside its send buffer (the
+ * all_to_all_single layout); they are never transferred. */
+int fast_plan_compile(const int64_t *D, const int64_t *send_self, int n, int m,
                       const fast_sched_bufs *sched, int64_t recv_capacity,
                       int64_t staging_capacity, const fast_plan *plan,
                       void *stream);
@@ -155,7 +158,8 @@ int fast_plan_compile(const int64_t *D, int n, int m,
 /* Same plan logic on HOST pointers -- validation/inspection only (CPU
  * tests); the executor never calls it.  `order/perm/sbytes` are one
  * matrix's packed stage arrays, K = n*n-2n+2. */
-int fast_plan_compile_host(const int64_t *D, int n, int m, int n_stages,
+int fast_plan_compile_host(const int64_t *D, const int64_t *send_self, int n,
+                           int m, int n_stages,
                            const int32_t *order, const uint8_t *perm,
                            const int64_t *sbytes, int64_t recv_capacity,
                            int64_t staging_capacity, fast_op *ops,
@@ -176,13 +180,14 @@ int fast_comm_open_peers(fast_comm *c, const void *handles);
 int fast_comm_destroy(fast_comm *c);
 void *fast_comm_recv_ptr(const fast_comm *c);
 void *fast_comm_staging_ptr(const fast_comm *c);
-/* demand-matrix buffer of call `epoch` (double-buffered by parity) */
+/* demand-matrix buffer of call `epoch` (double-buffered by parity): G x G
+ * int64 with zero diagonal, followed by G int64 self-segment sizes */
 int64_t *fast_comm_demand_ptr(const fast_comm *c, int64_t epoch);
 int64_t fast_comm_recv_capacity(const fast_comm *c);
 int64_t fast_comm_staging_capacity(const fast_comm *c);
 
-/* All-gather of this rank's demand row (int64[world], device) into every
- * rank's demand buffer for `epoch` (>= 1, +1 per call): P2P writes + a
+/* All-gather of this rank's demand row (int64[world], device; entry `rank`
+ * = bytes of its own segment, kept local) into every rank's demand buffer for `epoch` (>= 1, +1 per call): P2P writes + a
  * release counter; returns after the local matrix is complete (on the
  * device, stream-ordered).  Replaces Megatron's count all-gather
  * (PAPER.md:617-619). */

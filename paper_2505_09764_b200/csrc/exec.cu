@@ -182,11 +182,14 @@ __global__ void gather_demand_kernel(uint8_t* const* peers, const int64_t* row,
                                      int64_t epoch, int rank, int world,
                                      int64_t demand_off) {
   // lane r (< world) writes this rank's row into rank r's demand buffer
+  // row[rank] (self bytes) goes to the self-size vector, D keeps a zero
+  // diagonal (DemandMatrix invariant, model.py:97-98)
   const int G = world;
   const int par = (int)(epoch & 1);
   for (int r = threadIdx.x; r < world; r += blockDim.x) {
-    int64_t* dm = reinterpret_cast<int64_t*>(peers[r] + demand_off) + (int64_t)par * G * G;
-    for (int h = 0; h < G; ++h) dm[(int64_t)rank * G + h] = row[h];
+    int64_t* dm = reinterpret_cast<int64_t*>(peers[r] + demand_off) + (int64_t)par * (G * G + G);
+    for (int h = 0; h < G; ++h) dm[(int64_t)rank * G + h] = h == rank ? 0 : row[h];
+    dm[(int64_t)G * G + rank] = row[rank];
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -330,15 +333,16 @@ int64_t fast_plan_op_capacity(int n, int m) {
   return fastplan::plan_op_capacity(n, m, n * n - 2 * n + 2);
 }
 
-int fast_plan_compile(const int64_t* D, int n, int m, const fast_sched_bufs* sched,
-                      int64_t recv_capacity, int64_t staging_capacity,
-                      const fast_plan* plan, void* stream) {
+int fast_plan_compile(const int64_t* D, const int64_t* send_self, int n, int m,
+                      const fast_sched_bufs* sched, int64_t recv_capacity,
+                      int64_t staging_capacity, const fast_plan* plan, void* stream) {
   if (!sched || !plan || n < 2 || m < 1 || m > FAST_MAX_GPUS_PER_SERVER) return FAST_EVALIDATION;
   fastplan::PlanIn in;
   in.n = n;
   in.m = m;
   in.K = n * n - 2 * n + 2;
   in.D = D;
+  in.send_self = send_self;
   in.n_stages = -1;  // read on the device
   in.order = sched->stage_order;
   in.perm = sched->stage_perm;
@@ -357,7 +361,8 @@ int fast_plan_compile(const int64_t* D, int n, int m, const fast_sched_bufs* sch
   return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
 }
 
-int fast_plan_compile_host(const int64_t* D, int n, int m, int n_stages, const int32_t* order,
+int fast_plan_compile_host(const int64_t* D, const int64_t* send_self, int n, int m,
+                           int n_stages, const int32_t* order,
                            const uint8_t* perm, const int64_t* sbytes, int64_t recv_capacity,
                            int64_t staging_capacity, fast_op* ops, int64_t op_capacity,
                            int32_t* n_ops, int64_t* staging_used, void* workspace) {
@@ -368,6 +373,7 @@ int fast_plan_compile_host(const int64_t* D, int n, int m, int n_stages, const i
   in.m = m;
   in.K = n * n - 2 * n + 2;
   in.D = D;
+  in.send_self = send_self;
   in.n_stages = n_stages;
   in.order = order;
   in.perm = perm;
@@ -398,12 +404,12 @@ int fast_comm_create(int rank, int world, int max_gpus_per_row, int64_t recv_byt
   c->recv_bytes = recv_bytes;
   c->staging_bytes = staging_bytes;
   c->demand_off = kFlagBytes;
-  c->recv_off = fastplan::align16(c->demand_off + 2 * (int64_t)world * world * 8 + 256);
+  c->recv_off = fastplan::align16(c->demand_off + 2 * ((int64_t)world * world + world) * 8 + 256);
   c->recv_off = (c->recv_off + 4095) & ~(int64_t)4095;
   c->staging_off = (c->recv_off + recv_bytes + 64 + 4095) & ~(int64_t)4095;
   c->total = (c->staging_off + staging_bytes + 64 + 4095) & ~(int64_t)4095;
   if (cudaMalloc(&c->base, (size_t)c->total) != cudaSuccess) { free(c); return FAST_ECUDA; }
-  if (cudaMemset(c->base, 0, (size_t)kFlagBytes + 2 * (size_t)world * world * 8) != cudaSuccess ||
+  if (cudaMemset(c->base, 0, (size_t)c->recv_off) != cudaSuccess ||
       cudaIpcGetMemHandle(&c->handle, c->base) != cudaSuccess) {
     cudaFree(c->base);
     free(c);
@@ -465,7 +471,7 @@ void* fast_comm_staging_ptr(const fast_comm* c) { return c ? c->base + c->stagin
 int64_t* fast_comm_demand_ptr(const fast_comm* c, int64_t epoch) {
   if (!c) return nullptr;
   return reinterpret_cast<int64_t*>(c->base + c->demand_off) +
-         (epoch & 1) * (int64_t)c->world * c->world;
+         (epoch & 1) * ((int64_t)c->world * c->world + c->world);
 }
 int64_t fast_comm_recv_capacity(const fast_comm* c) { return c ? c->recv_bytes : 0; }
 int64_t fast_comm_staging_capacity(const fast_comm* c) { return c ? c->staging_bytes : 0; }

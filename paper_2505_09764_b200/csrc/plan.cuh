@@ -68,7 +68,9 @@ FAST_HD inline int64_t plan_op_capacity(int n, int m, int K) {
 
 struct PlanIn {
   int n, m, K;               // servers, gpus/server, stage capacity
-  const int64_t* D;          // [G][G]
+  const int64_t* D;          // [G][G], zero diagonal
+  const int64_t* send_self;  // [G] bytes of g's own segment kept in send_g
+                             // (all_to_all_single layout); may be null
   int n_stages;              // sorted kept stages
   const int32_t* order;      // [n_stages] raw stage index
   const uint8_t* perm;       // [K][n]
@@ -239,12 +241,13 @@ FAST_HD inline void plan_compile(const PlanIn& in, const PlanOut& out) {
   int status = FAST_OK;
 
   if (in.n_stages > 255 || m > FAST_MAX_GPUS_PER_SERVER) status = FAST_EVALIDATION;
-  // segment offsets
+  // segment offsets (the self segment, if any, stays in place in send_g)
   for (int g = 0; g < G; ++g) {
     int64_t a = 0;
     for (int h = 0; h < G; ++h) {
       w.send_off[(int64_t)g * G + h] = a;
       a += in.D[(int64_t)g * G + h];
+      if (h == g && in.send_self) a += in.send_self[g];
     }
   }
   for (int h = 0; h < G; ++h) {

@@ -93,7 +93,8 @@ class PlanBuffers:
 
 
 def plan_compile_host(D: np.ndarray, n: int, m: int, order: np.ndarray, perm: np.ndarray,
-                      sbytes: np.ndarray, recv_cap: int, staging_cap: int):
+                      sbytes: np.ndarray, recv_cap: int, staging_cap: int,
+                      send_self: np.ndarray | None = None):
     """Host build of the plan logic (validation / inspection only)."""
     lib = _lib.load()
     D = np.ascontiguousarray(D, dtype=np.int64)
@@ -109,7 +110,9 @@ def plan_compile_host(D: np.ndarray, n: int, m: int, order: np.ndarray, perm: np
     used = np.zeros(n * m, np.int64)
     ws = np.zeros(int(lib.fast_plan_workspace_bytes(n, m)) + 16, np.uint8)
     p = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
-    st = lib.fast_plan_compile_host(p(D), n, m, int(order.shape[0]), p(order), p(perm_k),
+    ss = None if send_self is None else np.ascontiguousarray(send_self, dtype=np.int64)
+    st = lib.fast_plan_compile_host(p(D), None if ss is None else p(ss), n, m,
+                                    int(order.shape[0]), p(order), p(perm_k),
                                     p(sb_k), int(recv_cap), int(staging_cap), p(ops), cap,
                                     p(n_ops), p(used), p(ws))
     return ops[: int(n_ops[0])].copy(), used, int(st)
@@ -151,7 +154,8 @@ class FastComm:
                       "fast_comm_create")
         self._ptr = ptr
         h = (ctypes.c_uint8 * 64)()
-        _lib.check_rc(lib.fast_comm_ipc_handle(ptr, h), "fast_comm_ipc_handle")
+        _lib.check_rc(lib.fast_comm_ipc_handle(ptr, ctypes.cast(h, ctypes.c_void_p)),
+                      "fast_comm_ipc_handle")
         handles: list = [None] * self.world
         dist.all_gather_object(handles, bytes(h), group=group)
         blob = b"".join(handles)
@@ -182,18 +186,23 @@ class FastComm:
         G = self.world
         return bytes_view(ptr, G * G * 8, self.device).view(torch.int64).view(G, G)
 
+    def self_sizes(self) -> torch.Tensor:
+        lib = _lib.load()
+        ptr = lib.fast_comm_demand_ptr(self._ptr, self.epoch) + 8 * self.world * self.world
+        return bytes_view(ptr, self.world * 8, self.device).view(torch.int64)
+
     def alltoallv(self, send: torch.Tensor, send_counts: torch.Tensor,
                   stream: torch.cuda.Stream | None = None, record_timeline: bool = False
                   ) -> torch.Tensor:
         """FAST alltoallv of `send` (uint8, device) split by send_counts
-        (int64[world] device, bytes per destination, own entry ignored).
+        (int64[world] device, bytes per destination in send order; the own
+        entry is the self segment, which stays in place and is not moved).
         Returns the recv region (source-major segments, self excluded)."""
         lib = _lib.load()
         if send.dtype != torch.uint8 or not send.is_cuda:
             raise ValidationError("send must be a cuda uint8 tensor")
         n, m = self.topology.n_servers, self.topology.gpus_per_server
-        row = send_counts.to(device=self.device, dtype=torch.int64).clone()
-        row[self.rank] = 0
+        row = send_counts.to(device=self.device, dtype=torch.int64).contiguous()
         self._row = row  # keep alive until the stream consumes it
         self.epoch += 1
         sh = _stream_handle(stream)
@@ -202,7 +211,8 @@ class FastComm:
         dptr = lib.fast_comm_demand_ptr(self._ptr, self.epoch)
         _lib.check_rc(lib.fast_synth_batch(ctypes.c_void_p(dptr), 1, n, m,
                                            ctypes.byref(self.sched.struct), sh), "fast_synth_batch")
-        _lib.check_rc(lib.fast_plan_compile(ctypes.c_void_p(dptr), n, m,
+        sself = ctypes.c_void_p(dptr + 8 * self.world * self.world)
+        _lib.check_rc(lib.fast_plan_compile(ctypes.c_void_p(dptr), sself, n, m,
                                             ctypes.byref(self.sched.struct), self.recv_bytes,
                                             self.staging_bytes, ctypes.byref(self.plan.struct), sh),
                       "fast_plan_compile")
@@ -314,7 +324,7 @@ class GroupComm:
         dp = ctypes.c_void_p(self._D.data_ptr())
         _lib.check_rc(lib.fast_synth_batch(dp, 1, n, m, ctypes.byref(self.sched.struct), sh),
                       "fast_synth_batch")
-        _lib.check_rc(lib.fast_plan_compile(dp, n, m, ctypes.byref(self.sched.struct),
+        _lib.check_rc(lib.fast_plan_compile(dp, None, n, m, ctypes.byref(self.sched.struct),
                                             self.recv_bytes, self.staging_bytes,
                                             ctypes.byref(self.plan.struct), sh),
                       "fast_plan_compile")

@@ -127,3 +127,27 @@ def test_plan_rejects_small_buffers():
     _, _, st = plan_compile_host(D, n, m, p.stage_order, p.stage_perm, p.stage_bytes,
                                  1 << 20, 0)
     assert st == 2
+
+
+def test_plan_self_segments_stay_in_place():
+    """all_to_all_single layout: send_g keeps its own segment in place."""
+    rng = np.random.default_rng(3)
+    for n, m in [(2, 1), (2, 4), (4, 2)]:
+        G = n * m
+        D = workloads.zipf_sizes(9, G, 1.1, 400_009)
+        selfb = rng.integers(0, 5000, G).astype(np.int64)
+        out = oracle.synthesize_batch(D, n, m)
+        p = PackedSchedule(**oracle.packed_fields(out, 0, n, m))
+        cap = int(D.sum(axis=0).max()) + 16
+        stg = int(D.sum()) + 1 << 16
+        ops, _, st = plan_compile_host(D, n, m, p.stage_order, p.stage_perm, p.stage_bytes,
+                                       cap, stg, send_self=selfb)
+        assert st == 0
+        Dfull = D + np.diag(selfb)
+        sends = [payload(g, int(Dfull[g].sum())) for g in range(G)]
+        got = replay(ops, sends, G, cap, stg)
+        full = direct_alltoallv(sends, Dfull)
+        for h in range(G):
+            lo = int(Dfull[:h, h].sum())
+            want = np.concatenate([full[h][:lo], full[h][lo + selfb[h]:]])
+            assert np.array_equal(got[h][:len(want)], want), (n, m, h)
