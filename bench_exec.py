@@ -1,0 +1,256 @@
+"""alltoallv benchmark for bench.py at N > 1 (torchrun, one rank per GPU).
+
+Workload (BASELINE config 2 shape): Zipf alpha=1.2 traffic matrix with a
+256 MiB total over the N GPUs, virtual servers 2 x N/2 (N=8: 2x4; --topo
+4x2 for the other partition).  One step = one FastComm.alltoallv: P2P
+demand all-gather + FAST synthesis + plan compile + P2P stage execution,
+all on the device.  Timed with CUDA events, max over ranks.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from bench import ClockSampler, measured_peaks
+
+PEER_GBS = 770.0      # measured B200 peer copy per direction (B200_PROFILING.md)
+NVLINK_NOMINAL = 900.0
+
+
+def topology_for(world: int, spec: str | None):
+    if spec:
+        n, m = (int(x) for x in spec.lower().split("x"))
+        return n, m
+    return (2, world // 2) if world >= 2 else (1, 1)
+
+
+def demand(args, world: int) -> np.ndarray:
+    from paper_2505_09764_b200 import workloads
+
+    return workloads.zipf_sizes(args.seed, world, args.a2a_skew, args.a2a_total)
+
+
+def fast_wire_bytes(ops: np.ndarray, G: int) -> tuple[int, int]:
+    eg = np.zeros(G, np.int64)
+    ing = np.zeros(G, np.int64)
+    for o in ops:
+        if int(o["exec_rank"]) != int(o["dst_rank"]):
+            eg[int(o["exec_rank"])] += int(o["len"])
+            ing[int(o["dst_rank"])] += int(o["len"])
+    return int(eg.max()), int(ing.max())
+
+
+def run(args, workload: str) -> dict | None:
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        return reference_alltoallv(args, world) if rank == 0 else None
+    if world < 2:
+        return {"metric": "alltoallv algbw", "unavailable": "alltoallv needs >= 2 ranks (torchrun)"}
+    from paper_2505_09764_b200 import Topology, algorithmic_bandwidth
+    from paper_2505_09764_b200.executor import FastComm
+
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, m = topology_for(world, args.topo)
+    D = demand(args, world)
+    G = world
+    total = int(D.sum())
+    cap = int(max(D.sum(0).max(), D.sum(1).max())) + 4096
+    comm = FastComm(Topology(n, m), recv_bytes=cap, staging_bytes=2 * cap + (4 << 20),
+                    blocks=args.blocks, chunk_bytes=args.chunk)
+    row = torch.from_numpy(D[rank].copy()).cuda()
+    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    send = torch.randint(0, 256, (int(D[rank].sum()) + 16,), dtype=torch.uint8, device="cuda",
+                         generator=gen)
+    stream = torch.cuda.current_stream()
+
+    # correctness vs NCCL on the same bytes (not timed)
+    recv = comm.alltoallv(send, row)
+    nccl_out = torch.empty(int(D[:, rank].sum()), dtype=torch.uint8, device="cuda")
+    dist.all_to_all_single(nccl_out, send[: int(D[rank].sum())], D[:, rank].tolist(),
+                           D[rank].tolist())
+    torch.cuda.synchronize()
+    comm.check()
+    ok = torch.equal(recv[: nccl_out.numel()], nccl_out)
+    okt = torch.tensor([0 if ok else 1], device="cuda")
+    dist.all_reduce(okt)
+    if int(okt.item()) != 0:
+        raise RuntimeError("FAST alltoallv result differs from NCCL all_to_all_single")
+
+    for _ in range(args.warmup):
+        comm.alltoallv(send, row)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for k in range(args.steps):
+            comm.alltoallv(send, row, exec_events=ev[k])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    comm.check()
+    step_ms = t0.elapsed_time(t1) / args.steps
+    exec_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    mx = torch.tensor([step_ms, exec_ms], device="cuda")
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    step_ms, exec_ms = (float(x) for x in mx.tolist())
+
+    # NCCL all_to_all_single on the identical traffic (practical B200 bar)
+    ins, outs = D[rank].tolist(), D[:, rank].tolist()
+    sv = send[: int(D[rank].sum())]
+    for _ in range(args.warmup):
+        dist.all_to_all_single(nccl_out, sv, outs, ins)
+    torch.cuda.synchronize()
+    dist.barrier()
+    n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0.record(stream)
+    for _ in range(args.steps):
+        dist.all_to_all_single(nccl_out, sv, outs, ins)
+    n1.record(stream)
+    torch.cuda.synchronize()
+    nccl_ms = torch.tensor([n0.elapsed_time(n1) / args.steps], device="cuda")
+    dist.all_reduce(nccl_ms, op=dist.ReduceOp.MAX)
+    nccl_ms = float(nccl_ms.item())
+
+    # e2e through the public API with host buffers (pinned H2D + D2H per step)
+    host_send = torch.empty(send.numel(), dtype=torch.uint8, pin_memory=True)
+    host_send.copy_(send)
+    host_recv = torch.empty(int(D[:, rank].sum()), dtype=torch.uint8, pin_memory=True)
+    dsend = torch.empty_like(send)
+    for _ in range(2):
+        dsend.copy_(host_send, non_blocking=True)
+        r = comm.alltoallv(dsend, row)
+        host_recv.copy_(r[: host_recv.numel()], non_blocking=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        dsend.copy_(host_send, non_blocking=True)
+        r = comm.alltoallv(dsend, row)
+        host_recv.copy_(r[: host_recv.numel()], non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+    dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_ms.item())
+    comm.check()
+
+    ops = comm.plan.host_ops()
+    fast_eg, fast_in = fast_wire_bytes(ops, G)
+    direct_bn = int(max(D.sum(0).max(), D.sum(1).max()))
+    t_roof = direct_bn / (PEER_GBS * 1e9)
+    res = None
+    if rank == 0:
+        peaks, kind = measured_peaks()
+        achieved = direct_bn / (exec_ms * 1e-3) / 1e9
+        res = {
+            "metric": "alltoallv algorithmic bandwidth (FAST schedule, P2P over NVSwitch; "
+                      "whole job = algbw/GPU x N)",
+            "value": round(total / (step_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(step_ms, 4), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8",
+            "data": f"synthetic (Zipf {args.a2a_skew} traffic, seed {args.seed}, random payload)",
+            "config": {"workload": "config2_alltoallv", "virtual_servers": f"{n}x{m}",
+                       "total_bytes": total, "zipf_skew": args.a2a_skew,
+                       "bottleneck_gpu_bytes": direct_bn, "blocks_per_rank": args.blocks,
+                       "chunk_bytes": args.chunk,
+                       "l2": "payload per step %.0f MB; recv/staging are rewritten each step"
+                             % (total / 1e6)},
+            "algbw_gbps_per_gpu": round(algorithmic_bandwidth(total, G, step_ms * 1e-3) / 1e9, 3),
+            "exec_kernel_ms": round(exec_ms, 4),
+            "synth_and_plan_ms": round(step_ms - exec_ms, 4),
+            "roofline": {"bound": "nvlink", "achieved": round(achieved, 2), "peak": PEER_GBS,
+                         "unit": "GB/s", "frac": round(t_roof / (exec_ms * 1e-3), 4),
+                         "traffic": None, "kernel": "exec_kernel",
+                         "peak_source": "measured B200 peer copy per direction "
+                                        "(B200_PROFILING.md); 900 GB/s nominal",
+                         "frac_of_nominal": round(direct_bn / (NVLINK_NOMINAL * 1e9) / (exec_ms * 1e-3), 4),
+                         "t_roof_us": round(t_roof * 1e6, 2),
+                         "fast_one_tier_ceiling": round(direct_bn / max(fast_eg, fast_in), 4),
+                         "fast_max_wire_bytes": max(fast_eg, fast_in),
+                         "frac_step": round(t_roof / (step_ms * 1e-3), 4)},
+            "nccl_all_to_all_single": {"ms": round(nccl_ms, 4),
+                                       "value": round(total / (nccl_ms * 1e-3) / 1e9, 3),
+                                       "unit": "GB/s"},
+            "e2e": {"value": round(total / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+                    "h2d_bytes_per_step": int(D[0].sum()) + 16,
+                    "d2h_bytes_per_step": int(D[:, 0].sum()), "ms_per_step": round(e2e_ms, 4),
+                    "path": "FastComm.alltoallv with pinned host send/recv (rank-0 bytes)"},
+            "gpu_launches": 6 * args.steps, "clocks": clk.summary(),
+            "parity": "recv == NCCL all_to_all_single bytes on every rank",
+        }
+    comm.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    return res
+
+
+def reference_alltoallv(args, world: int) -> dict:
+    """Reference arm: tiersched.synthesize_fast (baseline/_ref) + the host
+    memcpy alltoallv the schedule describes, on the host cores (rank 0)."""
+    import sys
+
+    from bench import REPO
+
+    G = max(world, 2)
+    n, m = topology_for(G, args.topo)
+    D = demand(args, G)
+    total = int(D.sum())
+    ref = os.path.join(REPO, "baseline", "_ref")
+    have = os.path.isdir(os.path.join(ref, "tiersched"))
+    if have:
+        sys.dont_write_bytecode = True
+        sys.path.insert(0, ref)
+        import tiersched as ts
+
+        def synth():
+            ts.synthesize_fast(ts.DemandMatrix(n, m, D.copy()), ts.Topology(n, m, 900e9, 900e9))
+        kind = "reference"
+    else:
+        from oracle import oracle
+
+        def synth():
+            oracle.synthesize_batch(D, n, m)
+        kind = "port"
+    from oracle.alltoallv import direct_alltoallv
+
+    rng = np.random.default_rng(0)
+    sends = [rng.integers(0, 256, int(D[g].sum()), dtype=np.uint8) for g in range(G)]
+
+    def step():
+        t = time.perf_counter()
+        synth()
+        direct_alltoallv(sends, D)
+        return time.perf_counter() - t
+
+    for _ in range(args.warmup):
+        step()
+    ts_ = [step() for _ in range(args.steps)]
+    sec = sum(ts_) / len(ts_)
+    val = total / sec / 1e9
+    return {"impl": "reference",
+            "metric": "alltoallv algorithmic bandwidth (FAST schedule, P2P over NVSwitch; "
+                      "whole job = algbw/GPU x N)",
+            "value": round(val, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "data": f"synthetic (Zipf {args.a2a_skew}, seed {args.seed})",
+            "config": {"workload": "config2_alltoallv", "virtual_servers": f"{n}x{m}",
+                       "total_bytes": total},
+            "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": 1, "kind": kind,
+                             "sample": "tiersched.synthesize_fast + host memcpy of every "
+                                       "segment (numpy, 1 thread), full 256 MiB per step"},
+            "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}

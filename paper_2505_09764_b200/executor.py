@@ -192,8 +192,8 @@ class FastComm:
         return bytes_view(ptr, self.world * 8, self.device).view(torch.int64)
 
     def alltoallv(self, send: torch.Tensor, send_counts: torch.Tensor,
-                  stream: torch.cuda.Stream | None = None, record_timeline: bool = False
-                  ) -> torch.Tensor:
+                  stream: torch.cuda.Stream | None = None, record_timeline: bool = False,
+                  exec_events: tuple | None = None) -> torch.Tensor:
         """FAST alltoallv of `send` (uint8, device) split by send_counts
         (int64[world] device, bytes per destination in send order; the own
         entry is the self segment, which stays in place and is not moved).
@@ -217,9 +217,13 @@ class FastComm:
                                             self.staging_bytes, ctypes.byref(self.plan.struct), sh),
                       "fast_plan_compile")
         tl = ctypes.c_void_p(self.timeline.data_ptr()) if record_timeline else None
+        if exec_events is not None:
+            exec_events[0].record(stream or torch.cuda.current_stream())
         _lib.check_rc(lib.fast_exec(self._ptr, ctypes.byref(self.plan.struct),
                                     ctypes.c_void_p(send.data_ptr()), self.epoch, self.blocks,
                                     self.chunk, tl, sh), "fast_exec")
+        if exec_events is not None:
+            exec_events[1].record(stream or torch.cuda.current_stream())
         return self.recv
 
     def check(self) -> None:
