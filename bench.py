@@ -355,8 +355,8 @@ def main() -> None:
     ap.add_argument("--a2a-skew", type=float, default=1.2)
     ap.add_argument("--a2a-total", type=int, default=268_435_456)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--blocks", type=int, default=32)
-    ap.add_argument("--chunk", type=int, default=256 * 1024)
+    ap.add_argument("--blocks", type=int, default=128)
+    ap.add_argument("--chunk", type=int, default=1024 * 1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()

@@ -483,10 +483,23 @@ int fast_gather_demand(fast_comm* c, const int64_t* row, int64_t epoch, void* st
   return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
 }
 
+// Every CTA of every rank must be resident at once (CTAs wait on flags that
+// other ranks' CTAs raise), so the grid may not exceed one wave.
+static int max_resident_blocks() {
+  int dev = 0, sms = 0, per_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, exec_kernel, kExecThreads, 0) !=
+          cudaSuccess)
+    return 0;
+  return sms * per_sm;
+}
+
 int fast_exec(fast_comm* c, const fast_plan* plan, const void* send, int64_t epoch, int blocks,
               int64_t chunk_bytes, int64_t* timeline_ns, void* stream) {
   if (!c || !c->opened || !plan || epoch < 1 || blocks < 1 || chunk_bytes < 16)
     return FAST_EVALIDATION;
+  if (blocks > max_resident_blocks()) return FAST_EVALIDATION;
   ExecArgs a;
   memset(&a, 0, sizeof(a));
   a.peers = c->peers_dev;
@@ -531,6 +544,7 @@ int fast_exec_group(fast_comm* const* comms, int world, const fast_plan* plan,
   if (!comms || world < 1 || world > kMaxRanks || !plan || epoch < 1 || blocks < 1 ||
       chunk_bytes < 16)
     return FAST_EVALIDATION;
+  if (blocks * world > max_resident_blocks()) return FAST_EVALIDATION;
   ExecArgs a;
   memset(&a, 0, sizeof(a));
   a.peers = comms[0]->peers_dev;

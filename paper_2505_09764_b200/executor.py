@@ -35,8 +35,8 @@ OP_DTYPE = np.dtype([("src_off", "<i8"), ("dst_off", "<i8"), ("len", "<i8"),
 PH_BALANCE, PH_DIRECT, PH_FROM_STAGING, PH_REDIST = 0, 1, 2, 3
 BUF_SEND, BUF_RECV, BUF_STAGING = 0, 1, 2
 TIMELINE_STRIDE = 8 + 256
-DEFAULT_BLOCKS = 32
-DEFAULT_CHUNK = 256 * 1024
+DEFAULT_BLOCKS = 128  # one 512-thread CTA per SM; must stay <= SM count (co-residency)
+DEFAULT_CHUNK = 1024 * 1024
 
 
 @dataclass(frozen=True)
