@@ -148,8 +148,9 @@ int64_t fast_plan_op_capacity(int n, int m);
 /* Plan compile on the device (one-thread kernel, stream-ordered): D [G][G]
  * (zero diagonal) and the packed schedule of matrix 0 of `sched` ->
  * phase-ordered ops.  send_self (device int64[G] or NULL): bytes of each
- * rank's own segment, kept in place inside its send buffer (the
- * all_to_all_single layout); they are never transferred. */
+ * rank's own segment, kept in place inside its send buffer and left as a
+ * gap at its slot of the receive buffer (the all_to_all_single layout on
+ * both sides); self bytes are never transferred. */
 int fast_plan_compile(const int64_t *D, const int64_t *send_self, int n, int m,
                       const fast_sched_bufs *sched, int64_t recv_capacity,
                       int64_t staging_capacity, const fast_plan *plan,
@@ -218,6 +219,44 @@ int fast_exec_group(fast_comm *const *comms, int world, const fast_plan *plan,
 /* Device status word of the last exec on this comm (0 ok, 3 = a wait timed
  * out: peers missing or protocol error). */
 int fast_comm_status(const fast_comm *c, int32_t *status_host);
+
+/* ------------------------------------------------------------------------
+ * MoE dispatch front-end (BASELINE config 3).  Absent from the reference
+ * (its traffic matrices are inputs); the paper takes them from Megatron's
+ * count all-gather.  Expert e lives on rank e (E = G).
+ * ------------------------------------------------------------------------ */
+
+/* Deterministic top-2 gating of T tokens: r1 = stream(seed)[t] >> 32,
+ * r2 = stream(seed)[T+t] >> 32; e1 = #{thr[i] <= r1}, e2 = #{thr2[e1][i] <= r2}
+ * (searchsorted 'right' on integer CDFs; thr2[e] has expert e's mass
+ * removed).  topk: int32 [T][2]. */
+int fast_moe_gate(int T, uint64_t seed, int E, const uint64_t *thr,
+                  const uint64_t *thr2, int32_t *topk, void *stream);
+
+/* Histogram + scan of the T*k routing entries (token order): stable rank of
+ * every entry inside its destination segment (pos), counts[E], segment row
+ * offsets seg_rows[E] (exclusive prefix) and the demand row in bytes
+ * (counts * row_bytes) -- this GPU's row of D.  workspace:
+ * fast_moe_route_workspace_bytes(T, k, E) bytes (per-block bases, read by
+ * fast_moe_pack). */
+size_t fast_moe_route_workspace_bytes(int T, int k, int E);
+int fast_moe_route(const int32_t *topk, int T, int k, int E, int64_t row_bytes,
+                   int32_t *pos, int64_t *counts, int64_t *seg_rows,
+                   int64_t *demand_row, void *workspace, void *stream);
+
+/* Pack: token t's row (row_bytes, 16-byte multiple) is copied to each of its
+ * k destination rows of `send` (grouped by destination, stable token
+ * order) -- the all_to_all_single send layout, self segment included. */
+int fast_moe_pack(const void *tokens, int T, int k, int64_t row_bytes,
+                  const int32_t *topk, const int32_t *pos, const void *workspace,
+                  int E, const int64_t *seg_rows, void *send, void *stream);
+
+/* Unpack: copy this rank's own segment from `send` into the gap the
+ * executor leaves at the self slot of `recv` (fast_plan_compile with
+ * send_self); recv then holds the expert input, source-major.  D and
+ * self_bytes are the gathered demand matrix / self sizes of the call. */
+int fast_moe_unpack_self(const int64_t *D, const int64_t *self_bytes, int G,
+                         int rank, const void *send, void *recv, void *stream);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,68 @@
+"""CPU ORACLE for the MoE dispatch front-end -- test infrastructure only.
+
+The reference has no MoE front-end; this restates the recipe
+of SURVEY.md 8(d) config 3 in numpy:
+  * gating: w_e = 1/((e - hot) mod E + 1)^alpha; integer CDF thresholds
+    thr = floor(cumsum(w)/sum(w) * 2^32), thr[E-1] = 2^32; for source s,
+    r = stream(seed*1000 + s, 2T) >> 32, e1 = searchsorted(thr, r[:T],
+    'right'), e2 = searchsorted(thr2[e1], r[T:], 'right') with thr2[e] the
+    thresholds of w with w[e] = 0;
+  * counts[s] = bincount(e1) + bincount(e2); D row = counts * row_bytes;
+  * pack: destination segments in expert order, tokens in ascending order;
+  * expert input on GPU h: source-major concat of every source's segment h.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from oracle.alltoallv import splitmix_stream
+
+
+def thresholds(E: int, alpha: float = 0.8, hot: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    w = 1.0 / (((np.arange(E) - hot) % E) + 1.0) ** alpha
+
+    def cdf(x):
+        t = np.floor(np.cumsum(x) / x.sum() * 2.0 ** 32).astype(np.uint64)
+        t[-1] = np.uint64(1 << 32)
+        return t
+
+    thr2 = np.stack([cdf(np.where(np.arange(E) == e, 0.0, w)) for e in range(E)])
+    return cdf(w), thr2
+
+
+def gate(seed: int, src: int, T: int, thr: np.ndarray, thr2: np.ndarray) -> np.ndarray:
+    r = splitmix_stream(seed * 1000 + src, 2 * T) >> np.uint64(32)
+    e1 = np.searchsorted(thr, r[:T], side="right")
+    e2 = (thr2[e1] <= r[T:, None]).sum(axis=1)
+    return np.stack([e1, e2], axis=1).astype(np.int32)
+
+
+def route(topk: np.ndarray, E: int):
+    flat = topk.reshape(-1)
+    counts = np.bincount(flat, minlength=E).astype(np.int64)
+    seg = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
+    order = np.argsort(flat, kind="stable")  # entries grouped by expert, token order
+    return counts, seg, order
+
+
+def pack(tokens: np.ndarray, topk: np.ndarray, E: int) -> np.ndarray:
+    """tokens [T, row_bytes] uint8 -> send rows [T*k, row_bytes]."""
+    _, _, order = route(topk, E)
+    k = topk.shape[1]
+    return tokens[order // k]
+
+
+def expert_inputs(tokens: list[np.ndarray], topks: list[np.ndarray], E: int) -> list[np.ndarray]:
+    """Expert input rows of every GPU h (source-major, self included)."""
+    G = len(tokens)
+    sends = [pack(tokens[s], topks[s], E) for s in range(G)]
+    segs = [route(topks[s], E) for s in range(G)]
+    out = []
+    for h in range(G):
+        parts = []
+        for s in range(G):
+            counts, seg, _ = segs[s]
+            parts.append(sends[s][seg[h]:seg[h] + counts[h]])
+        out.append(np.concatenate(parts))
+    return out

@@ -33,4 +33,10 @@ SIGNATURES: list[tuple[str, object, list]] = [
     ("fast_comm_status", I, [V, ctypes.POINTER(ctypes.c_int32)]),
     ("fast_comm_create_group", I, [I, I64, I64, ctypes.POINTER(V)]),
     ("fast_exec_group", I, [ctypes.POINTER(V), I, P_PLAN, ctypes.POINTER(V), I64, I, I64, V, V]),
+    # MoE front-end (moe.cu)
+    ("fast_moe_gate", I, [I, ctypes.c_uint64, I, V, V, V, V]),
+    ("fast_moe_route_workspace_bytes", ctypes.c_size_t, [I, I, I]),
+    ("fast_moe_route", I, [V, I, I, I, I64, V, V, V, V, V, V]),
+    ("fast_moe_pack", I, [V, I, I, I64, V, V, V, I, V, V, V]),
+    ("fast_moe_unpack_self", I, [V, V, I, I, V, V, V]),
 ]

@@ -1,0 +1,266 @@
+// moe.cu -- MoE dispatch front-end on B200 (sm_100a): the traffic-matrix
+// builder and token pack/unpack around the FAST alltoallv (BASELINE config
+// 3).  None of this exists in the reference ("MoE dispatch
+// front-end ... absent"); the paper obtains the matrix from Megatron's
+// all-gather of per-expert token counts.
+//
+//   moe_gate_kernel        deterministic top-k gating: SplitMix64 draws
+//                          compared against integer CDF thresholds (exact,
+//                          identical to the numpy oracle)
+//   moe_route_local_kernel stable counting-sort ranks: __match_any_sync per
+//                          warp, per-block expert totals
+//   moe_route_scan_kernel  block bases, counts, segment offsets, demand row
+//   moe_pack_kernel        one warp per token: the row is read once (16-B
+//                          vectors) and written to each of its k destination
+//                          rows of the send buffer (grouped by destination,
+//                          stable token order)
+//   moe_unpack_self_kernel the own segment goes from the send buffer into the
+//                          gap the executor leaves at the self slot of the
+//                          receive buffer, which then IS the expert input
+//                          (source-major, like all_to_all_single)
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fastb200.h"
+
+namespace {
+
+constexpr int kRouteThreads = 1024;
+constexpr int kMaxExperts = 64;
+
+__device__ __forceinline__ uint64_t splitmix(uint64_t seed, uint64_t k) {
+  uint64_t z = seed + (k + 1) * 0x9E3779B97F4A7C15ull;  // rng.py:20-44
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// searchsorted(thr, r, side="right") == #{i : thr[i] <= r}
+__device__ __forceinline__ int count_le(const uint64_t* thr, int E, uint64_t r) {
+  int c = 0;
+  for (int i = 0; i < E; ++i) c += thr[i] <= r ? 1 : 0;
+  return c;
+}
+
+__global__ void moe_gate_kernel(int T, uint64_t seed, int E, const uint64_t* __restrict__ thr,
+                                const uint64_t* __restrict__ thr2, int32_t* __restrict__ topk) {
+  __shared__ uint64_t s_thr[kMaxExperts], s_thr2[kMaxExperts * kMaxExperts];
+  for (int i = threadIdx.x; i < E; i += blockDim.x) s_thr[i] = thr[i];
+  for (int i = threadIdx.x; i < E * E; i += blockDim.x) s_thr2[i] = thr2[i];
+  __syncthreads();
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+    const uint64_t r1 = splitmix(seed, (uint64_t)t) >> 32;
+    const uint64_t r2 = splitmix(seed, (uint64_t)T + t) >> 32;
+    const int e1 = count_le(s_thr, E, r1);
+    const int e2 = count_le(s_thr2 + e1 * E, E, r2);
+    topk[2 * t] = e1;
+    topk[2 * t + 1] = e2;
+  }
+}
+
+// entries i = t*k + j in token order; pos[i] <- rank of i among the block's
+// entries with the same destination; blk[b][e] <- block totals
+__global__ void __launch_bounds__(kRouteThreads)
+    moe_route_local_kernel(const int32_t* __restrict__ topk, int N, int E,
+                           int32_t* __restrict__ pos, int32_t* __restrict__ blk) {
+  __shared__ int32_t wcnt[kRouteThreads / 32][kMaxExperts];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < (kRouteThreads / 32) * E; i += blockDim.x) (&wcnt[0][0])[(i / E) * kMaxExperts + i % E] = 0;
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + tid;
+  const int e = i < N ? topk[i] : -1;
+  const unsigned peers = __match_any_sync(0xffffffffu, e);
+  const int lrank = __popc(peers & ((1u << lane) - 1u));
+  if (e >= 0 && lrank == 0) wcnt[warp][e] = __popc(peers);
+  __syncthreads();
+  // exclusive prefix over warps, per expert; block total
+  if (tid < E) {
+    int run = 0;
+    for (int w = 0; w < kRouteThreads / 32; ++w) {
+      const int c = wcnt[w][tid];
+      wcnt[w][tid] = run;
+      run += c;
+    }
+    blk[(int64_t)blockIdx.x * E + tid] = run;
+  }
+  __syncthreads();
+  if (e >= 0) pos[i] = wcnt[warp][e] + lrank;
+}
+
+__global__ void moe_route_scan_kernel(int nblocks, int E, int64_t row_bytes,
+                                      int32_t* __restrict__ blk, int64_t* __restrict__ counts,
+                                      int64_t* __restrict__ seg_rows,
+                                      int64_t* __restrict__ demand_row) {
+  __shared__ int64_t s_cnt[kMaxExperts];
+  const int e = threadIdx.x;
+  if (e < E) {
+    int64_t run = 0;
+    for (int b = 0; b < nblocks; ++b) {
+      const int c = blk[(int64_t)b * E + e];
+      blk[(int64_t)b * E + e] = (int32_t)run;  // becomes the block base
+      run += c;
+    }
+    s_cnt[e] = run;
+    counts[e] = run;
+    demand_row[e] = run * row_bytes;
+  }
+  __syncthreads();
+  if (e == 0) {
+    int64_t a = 0;
+    for (int x = 0; x < E; ++x) {
+      seg_rows[x] = a;
+      a += s_cnt[x];
+    }
+  }
+}
+
+__device__ __forceinline__ uint4 ldg_nc(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void stg_na(uint4* p, uint4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// one warp per token; row_vec = row_bytes / 16 (row_bytes % 16 == 0)
+template <int K>
+__global__ void __launch_bounds__(256)
+    moe_pack_kernel(const uint4* __restrict__ tokens, int T, int64_t row_vec,
+                    const int32_t* __restrict__ topk, const int32_t* __restrict__ pos,
+                    const int32_t* __restrict__ blkbase, int E,
+                    const int64_t* __restrict__ seg_rows, uint4* __restrict__ send) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp; t < T; t += nwarps) {
+    uint4* dst[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int i = t * K + j;
+      const int e = topk[i];
+      const int64_t row = seg_rows[e] + blkbase[(int64_t)(i / kRouteThreads) * E + e] + pos[i];
+      dst[j] = send + row * row_vec;
+    }
+    const uint4* src = tokens + (int64_t)t * row_vec;
+    constexpr int U = 4;
+    int64_t v = lane;
+    for (; v + (U - 1) * 32 < row_vec; v += U * 32) {
+      uint4 x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) x[u] = ldg_nc(src + v + u * 32);
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+#pragma unroll
+        for (int u = 0; u < U; ++u) stg_na(dst[j] + v + u * 32, x[u]);
+    }
+    for (; v < row_vec; v += 32) {
+      const uint4 x = ldg_nc(src + v);
+#pragma unroll
+      for (int j = 0; j < K; ++j) stg_na(dst[j] + v, x);
+    }
+  }
+}
+
+// own segment: send[sum_{h<rank} D[rank][h] ...] -> recv[sum_{g<rank} D[g][rank] ...]
+__global__ void moe_unpack_self_kernel(const int64_t* __restrict__ D,
+                                       const int64_t* __restrict__ self_bytes, int G, int rank,
+                                       const uint8_t* __restrict__ send, uint8_t* __restrict__ recv) {
+  int64_t soff = 0, roff = 0;
+  for (int h = 0; h < rank; ++h) soff += D[(int64_t)rank * G + h];
+  for (int g = 0; g < rank; ++g) roff += D[(int64_t)g * G + rank];
+  const int64_t len = self_bytes[rank];
+  const uint8_t* s = send + soff;
+  uint8_t* d = recv + roff;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  if ((((uintptr_t)s | (uintptr_t)d) & 15) == 0) {
+    const int64_t nv = len >> 4;
+    for (int64_t v = tid; v < nv; v += nt)
+      stg_na(reinterpret_cast<uint4*>(d) + v, ldg_nc(reinterpret_cast<const uint4*>(s) + v));
+    for (int64_t b = (nv << 4) + tid; b < len; b += nt) d[b] = s[b];
+  } else {
+    for (int64_t b = tid; b < len; b += nt) d[b] = s[b];
+  }
+}
+
+int sm_count() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t fast_moe_route_workspace_bytes(int T, int k, int E) {
+  if (T < 0 || k < 1 || E < 1) return 0;
+  const int64_t N = (int64_t)T * k;
+  const int64_t nb = (N + kRouteThreads - 1) / kRouteThreads;
+  return (size_t)((nb > 0 ? nb : 1) * E * 4);
+}
+
+int fast_moe_gate(int T, uint64_t seed, int E, const uint64_t* thr, const uint64_t* thr2,
+                  int32_t* topk, void* stream) {
+  if (T < 0 || E < 2 || E > kMaxExperts || !thr || !thr2 || !topk) return FAST_EVALIDATION;
+  if (T == 0) return FAST_OK;
+  const int blocks = (T + 255) / 256 < 4 * sm_count() ? (T + 255) / 256 : 4 * sm_count();
+  moe_gate_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(T, seed, E, thr, thr2, topk);
+  return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
+}
+
+int fast_moe_route(const int32_t* topk, int T, int k, int E, int64_t row_bytes, int32_t* pos,
+                   int64_t* counts, int64_t* seg_rows, int64_t* demand_row, void* workspace,
+                   void* stream) {
+  if (T < 0 || k < 1 || E < 1 || E > kMaxExperts || row_bytes < 0 || !counts || !seg_rows ||
+      !demand_row || !workspace)
+    return FAST_EVALIDATION;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int N = T * k;
+  const int nb = N > 0 ? (N + kRouteThreads - 1) / kRouteThreads : 0;
+  if (nb > 0)
+    moe_route_local_kernel<<<nb, kRouteThreads, 0, s>>>(topk, N, E, pos, (int32_t*)workspace);
+  moe_route_scan_kernel<<<1, 64, 0, s>>>(nb, E, row_bytes, (int32_t*)workspace, counts,
+                                         seg_rows, demand_row);
+  return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
+}
+
+int fast_moe_pack(const void* tokens, int T, int k, int64_t row_bytes, const int32_t* topk,
+                  const int32_t* pos, const void* workspace, int E, const int64_t* seg_rows,
+                  void* send, void* stream) {
+  if (T < 0 || (k != 1 && k != 2 && k != 4 && k != 8) || row_bytes <= 0 || (row_bytes & 15) ||
+      ((uintptr_t)tokens & 15) || ((uintptr_t)send & 15))
+    return FAST_EVALIDATION;
+  if (T == 0) return FAST_OK;
+  const int threads = 256;
+  int blocks = (int)(((int64_t)T * 32 + threads - 1) / threads);
+  if (blocks > 8 * sm_count()) blocks = 8 * sm_count();
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t rv = row_bytes / 16;
+  const uint4* tk = (const uint4*)tokens;
+  uint4* sd = (uint4*)send;
+  const int32_t* bb = (const int32_t*)workspace;
+  switch (k) {
+    case 1: moe_pack_kernel<1><<<blocks, threads, 0, s>>>(tk, T, rv, topk, pos, bb, E, seg_rows, sd); break;
+    case 2: moe_pack_kernel<2><<<blocks, threads, 0, s>>>(tk, T, rv, topk, pos, bb, E, seg_rows, sd); break;
+    case 4: moe_pack_kernel<4><<<blocks, threads, 0, s>>>(tk, T, rv, topk, pos, bb, E, seg_rows, sd); break;
+    default: moe_pack_kernel<8><<<blocks, threads, 0, s>>>(tk, T, rv, topk, pos, bb, E, seg_rows, sd); break;
+  }
+  return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
+}
+
+int fast_moe_unpack_self(const int64_t* D, const int64_t* self_bytes, int G, int rank,
+                         const void* send, void* recv, void* stream) {
+  if (!D || !self_bytes || G < 1 || rank < 0 || rank >= G || !send || !recv)
+    return FAST_EVALIDATION;
+  moe_unpack_self_kernel<<<2 * sm_count(), 512, 0, (cudaStream_t)stream>>>(
+      D, self_bytes, G, rank, (const uint8_t*)send, (uint8_t*)recv);
+  return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
+}
+
+}  // extern "C"

@@ -250,11 +250,15 @@ FAST_HD inline void plan_compile(const PlanIn& in, const PlanOut& out) {
       if (h == g && in.send_self) a += in.send_self[g];
     }
   }
+  // recv_h is source-major; with send_self the own segment's slot is left
+  // as a gap (filled locally, e.g. by the MoE unpack), so recv_h is laid out
+  // exactly like all_to_all_single's output
   for (int h = 0; h < G; ++h) {
     int64_t a = 0;
     for (int g = 0; g < G; ++g) {
       w.recv_off[(int64_t)g * G + h] = a;
       a += in.D[(int64_t)g * G + h];
+      if (g == h && in.send_self) a += in.send_self[h];
     }
     if (a > in.recv_cap) status = FAST_EVALIDATION;
   }

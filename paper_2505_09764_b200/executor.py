@@ -197,7 +197,9 @@ class FastComm:
         """FAST alltoallv of `send` (uint8, device) split by send_counts
         (int64[world] device, bytes per destination in send order; the own
         entry is the self segment, which stays in place and is not moved).
-        Returns the recv region (source-major segments, self excluded)."""
+        Returns the recv region: source-major segments exactly like
+        all_to_all_single's output, except that the own segment's slot is a
+        gap of send_counts[rank] bytes (never transferred; fill it locally)."""
         lib = _lib.load()
         if send.dtype != torch.uint8 or not send.is_cuda:
             raise ValidationError("send must be a cuda uint8 tensor")
@@ -260,20 +262,28 @@ def all_to_all_fast(output: torch.Tensor, input: torch.Tensor,
     counts = torch.tensor([s * row_bytes for s in input_split_sizes], dtype=torch.int64,
                           device=input.device)
     recv = comm.alltoallv(inb, counts)
+    # recv is laid out like all_to_all_single's output with a gap at the self
+    # slot: one contiguous copy, then the local segment into its slot
     outb = output.view(torch.uint8).reshape(-1)
     r = comm.rank
+    total_out = sum(output_split_sizes) * row_bytes
     self_in = sum(input_split_sizes[:r]) * row_bytes
     self_out = sum(output_split_sizes[:r]) * row_bytes
     nself = input_split_sizes[r] * row_bytes
-    before = self_out
-    after = sum(output_split_sizes[r + 1:]) * row_bytes
-    if before:
-        outb[:before].copy_(recv[:before])
+    if total_out:
+        outb[:total_out].copy_(recv[:total_out])
     if nself:
         outb[self_out:self_out + nself].copy_(inb[self_in:self_in + nself])
-    if after:
-        outb[self_out + nself:self_out + nself + after].copy_(recv[before:before + after])
     return output
+
+
+class GroupRank:
+    """Rank view of a GroupComm (world, rank, device) for per-rank helpers
+    such as MoEDispatch in single-GPU tests."""
+
+    def __init__(self, group: "GroupComm", rank: int):
+        self.world, self.rank, self.device = group.world, rank, group.device
+        self.recv = group.recvs[rank]
 
 
 class GroupComm:
@@ -317,18 +327,24 @@ class GroupComm:
             pass
 
     def alltoallv(self, sends: list[torch.Tensor], D: torch.Tensor,
-                  stream: torch.cuda.Stream | None = None) -> list[torch.Tensor]:
+                  stream: torch.cuda.Stream | None = None,
+                  self_bytes: torch.Tensor | None = None) -> list[torch.Tensor]:
+        """D: [world, world] int64, zero diagonal.  self_bytes (optional,
+        int64[world]): own segments kept in place in send_g and left as a
+        gap in recv_g (all_to_all_single layout)."""
         lib = _lib.load()
         n, m = self.topology.n_servers, self.topology.gpus_per_server
         if D.dtype != torch.int64 or tuple(D.shape) != (self.world, self.world):
             raise ValidationError("D must be int64 [world, world]")
         self._D = D.to(self.device).contiguous()
+        self._self = None if self_bytes is None else self_bytes.to(self.device, torch.int64).contiguous()
         self.epoch += 1
         sh = _stream_handle(stream)
         dp = ctypes.c_void_p(self._D.data_ptr())
         _lib.check_rc(lib.fast_synth_batch(dp, 1, n, m, ctypes.byref(self.sched.struct), sh),
                       "fast_synth_batch")
-        _lib.check_rc(lib.fast_plan_compile(dp, None, n, m, ctypes.byref(self.sched.struct),
+        sp_self = None if self._self is None else ctypes.c_void_p(self._self.data_ptr())
+        _lib.check_rc(lib.fast_plan_compile(dp, sp_self, n, m, ctypes.byref(self.sched.struct),
                                             self.recv_bytes, self.staging_bytes,
                                             ctypes.byref(self.plan.struct), sh),
                       "fast_plan_compile")

@@ -1,0 +1,111 @@
+"""MoE dispatch front-end: gating -> histogram/scan -> pack -> FAST
+alltoallv -> unpack, all on the device (BASELINE config 3).
+
+    disp = MoEDispatch(comm, tokens_per_gpu=16384, row_bytes=8192)
+    expert_in = disp.dispatch(tokens, seed=0)   # [recv rows, row_bytes] uint8
+
+Expert e lives on rank e (E = world).  The receive region of the executor is
+laid out like all_to_all_single's output with a gap at the self slot; the
+unpack kernel copies the local segment into that gap, so the receive region
+IS the expert input (source-major, stable token order within a source).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .model import ValidationError
+from .synth import _stream_handle
+
+
+def gating_thresholds(E: int, alpha: float = 0.8, hot: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    """Integer CDF thresholds of w_e = 1/((e-hot) mod E + 1)^alpha (top-1) and,
+    per first choice e, of w with w[e] = 0 (top-2)."""
+    w = 1.0 / (((np.arange(E) - hot) % E) + 1.0) ** alpha
+
+    def cdf(x):
+        t = np.floor(np.cumsum(x) / x.sum() * 2.0 ** 32).astype(np.uint64)
+        t[-1] = np.uint64(1 << 32)
+        return t
+
+    return cdf(w), np.stack([cdf(np.where(np.arange(E) == e, 0.0, w)) for e in range(E)])
+
+
+class MoEDispatch:
+    """Device buffers + the five kernels of one MoE dispatch (one rank)."""
+
+    def __init__(self, comm, tokens_per_gpu: int, row_bytes: int, k: int = 2,
+                 alpha: float = 0.8):
+        if row_bytes % 16:
+            raise ValidationError("row_bytes must be a multiple of 16")
+        if k != 2:
+            raise ValidationError("the synthetic gate is top-2")
+        self.comm = comm
+        self.T, self.row_bytes, self.k = tokens_per_gpu, row_bytes, k
+        self.E = comm.world
+        dev = comm.device
+        lib = _lib.load()
+        self.topk = torch.empty(self.T * k, dtype=torch.int32, device=dev)
+        self.pos = torch.empty(self.T * k, dtype=torch.int32, device=dev)
+        self.counts = torch.empty(self.E, dtype=torch.int64, device=dev)
+        self.seg_rows = torch.empty(self.E, dtype=torch.int64, device=dev)
+        self.demand_row = torch.empty(self.E, dtype=torch.int64, device=dev)
+        self.ws = torch.empty(max(16, int(lib.fast_moe_route_workspace_bytes(self.T, k, self.E))),
+                              dtype=torch.uint8, device=dev)
+        self.send = torch.empty(self.T * k * row_bytes, dtype=torch.uint8, device=dev)
+        self.set_hot(0, alpha)
+
+    def set_hot(self, hot: int, alpha: float = 0.8) -> None:
+        thr, thr2 = gating_thresholds(self.E, alpha, hot)
+        self.thr = torch.from_numpy(thr.view(np.int64)).to(self.comm.device)
+        self.thr2 = torch.from_numpy(np.ascontiguousarray(thr2).view(np.int64)).to(self.comm.device)
+
+    def route(self, seed: int, stream=None) -> None:
+        """gating + histogram/scan (the traffic-matrix builder, row of D)."""
+        lib = _lib.load()
+        sh = _stream_handle(stream)
+        P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        _lib.check_rc(lib.fast_moe_gate(self.T, ctypes.c_uint64(seed * 1000 + self.comm.rank),
+                                        self.E, P(self.thr), P(self.thr2), P(self.topk), sh),
+                      "fast_moe_gate")
+        _lib.check_rc(lib.fast_moe_route(P(self.topk), self.T, self.k, self.E, self.row_bytes,
+                                         P(self.pos), P(self.counts), P(self.seg_rows),
+                                         P(self.demand_row), P(self.ws), sh), "fast_moe_route")
+
+    def pack(self, tokens: torch.Tensor, stream=None) -> None:
+        lib = _lib.load()
+        P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        if tokens.numel() * tokens.element_size() != self.T * self.row_bytes:
+            raise ValidationError("tokens must be [T, row_bytes] worth of data")
+        _lib.check_rc(lib.fast_moe_pack(P(tokens), self.T, self.k, self.row_bytes, P(self.topk),
+                                        P(self.pos), P(self.ws), self.E, P(self.seg_rows),
+                                        P(self.send), _stream_handle(stream)), "fast_moe_pack")
+
+    def unpack(self, stream=None, D: torch.Tensor | None = None,
+               self_sizes: torch.Tensor | None = None, recv: torch.Tensor | None = None
+               ) -> torch.Tensor:
+        """Copy the own segment into the self slot of the receive region.
+        D / self_sizes / recv default to the communicator's last call."""
+        lib = _lib.load()
+        c = self.comm
+        D = c.demand() if D is None else D
+        ss = c.self_sizes() if self_sizes is None else self_sizes
+        recv = c.recv if recv is None else recv
+        _lib.check_rc(lib.fast_moe_unpack_self(ctypes.c_void_p(D.data_ptr()),
+                                               ctypes.c_void_p(ss.data_ptr()), c.world, c.rank,
+                                               ctypes.c_void_p(self.send.data_ptr()),
+                                               ctypes.c_void_p(recv.data_ptr()),
+                                               _stream_handle(stream)), "fast_moe_unpack_self")
+        return recv
+
+    def dispatch(self, tokens: torch.Tensor, seed: int, stream=None) -> torch.Tensor:
+        """Full dispatch; returns the receive region (expert input rows,
+        source-major; the row count is counts summed over sources)."""
+        self.route(seed, stream)
+        self.pack(tokens, stream)
+        self.comm.alltoallv(self.send, self.demand_row, stream=stream)
+        return self.unpack(stream)

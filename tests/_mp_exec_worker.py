@@ -75,6 +75,26 @@ def main() -> int:
         if not torch.equal(y_fast.view(torch.int16), y_nccl.view(torch.int16)):
             print(f"[rank {rank}] all_to_all_fast != all_to_all_single (n={n}, m={m})", flush=True)
             ok = False
+        # MoE dispatch (config 3 shape, scaled): expert inputs vs the oracle
+        from oracle import moe as moe_oracle
+        from paper_2505_09764_b200.moe import MoEDispatch, gating_thresholds
+
+        T, RB = 2048, 8192
+        mcomm = FastComm(Topology(n, m), recv_bytes=2 * T * RB * 3, staging_bytes=2 * T * RB * 3,
+                         blocks=64)
+        disp = MoEDispatch(mcomm, T, RB)
+        toks = [payload(500 + s, T * RB).reshape(T, RB) for s in range(world)]
+        recv = disp.dispatch(torch.from_numpy(toks[rank]).cuda(), seed=1)
+        torch.cuda.synchronize()
+        mcomm.check()
+        thr, thr2 = gating_thresholds(world)
+        topks = [moe_oracle.gate(1, s, T, thr, thr2) for s in range(world)]
+        want = moe_oracle.expert_inputs(toks, topks, world)[rank]
+        got = recv[: want.size].cpu().numpy().reshape(-1, RB)
+        if not np.array_equal(got, want):
+            print(f"[rank {rank}] MoE expert input mismatch (n={n}, m={m})", flush=True)
+            ok = False
+        mcomm.close()
         comm.close()
         dist.barrier()
     flag = torch.tensor([0 if ok else 1], device="cuda")
