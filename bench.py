@@ -357,6 +357,8 @@ def main() -> None:
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--blocks", type=int, default=128)
     ap.add_argument("--chunk", type=int, default=1024 * 1024)
+    ap.add_argument("--tokens", type=int, default=16384)
+    ap.add_argument("--hidden", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -375,8 +377,9 @@ def main() -> None:
         print(json.dumps(res), flush=True)
         return
     from bench_exec import run as run_exec
+    from bench_exec import run_moe
 
-    res = run_exec(args, workload)
+    res = run_moe(args) if workload == "moe" else run_exec(args, workload)
     if res is not None:
         print(json.dumps(res), flush=True)
 

@@ -254,3 +254,103 @@ def reference_alltoallv(args, world: int) -> dict:
                                        "segment (numpy, 1 thread), full 256 MiB per step"},
             "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+
+
+def run_moe(args) -> dict | None:
+    """BASELINE config 3: Mixtral-style dispatch, E = N experts (one per GPU),
+    top-2, 16k tokens x 4096 bf16 per GPU.  One step = gating -> histogram ->
+    demand all-gather -> FAST synthesis -> pack -> P2P alltoallv -> unpack."""
+    from paper_2505_09764_b200 import Topology
+    from paper_2505_09764_b200.executor import FastComm
+    from paper_2505_09764_b200.moe import MoEDispatch
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, m = topology_for(world, args.topo)
+    T, hidden = args.tokens, args.hidden
+    RB = hidden * 2
+    cap = T * 2 * RB * 2  # generous: a hot expert can receive 2x its share
+    comm = FastComm(Topology(n, m), recv_bytes=cap, staging_bytes=cap, blocks=args.blocks,
+                    chunk_bytes=args.chunk)
+    disp = MoEDispatch(comm, T, RB)
+    gen = torch.Generator(device="cuda").manual_seed(7 + rank)
+    tokens = torch.randn(T, hidden, dtype=torch.bfloat16, device="cuda", generator=gen)
+    stream = torch.cuda.current_stream()
+    recv = disp.dispatch(tokens, seed=args.seed)
+    torch.cuda.synchronize()
+    comm.check()
+    Dg = comm.demand().cpu().numpy() + np.diag(comm.self_sizes().cpu().numpy())
+    # NCCL bar: all_to_all_single of the same packed buffer (self included)
+    ins, outs = Dg[rank].tolist(), Dg[:, rank].tolist()
+    nsend = disp.send[: int(Dg[rank].sum())]
+    nccl_out = torch.empty(int(Dg[:, rank].sum()), dtype=torch.uint8, device="cuda")
+    dist.all_to_all_single(nccl_out, nsend, outs, ins)
+    torch.cuda.synchronize()
+    ok = torch.equal(recv[: nccl_out.numel()], nccl_out)
+    okt = torch.tensor([0 if ok else 1], device="cuda")
+    dist.all_reduce(okt)
+    if int(okt.item()) != 0:
+        raise RuntimeError("MoE expert input differs from NCCL all_to_all_single")
+    for _ in range(args.warmup):
+        disp.dispatch(tokens, seed=args.seed)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for _ in range(args.steps):
+            disp.dispatch(tokens, seed=args.seed)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    comm.check()
+    ms = torch.tensor([t0.elapsed_time(t1) / args.steps], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    # NCCL path: our route + pack, NCCL alltoall (no FAST), timed the same way
+    for _ in range(args.warmup):
+        disp.route(args.seed)
+        disp.pack(tokens)
+        dist.all_to_all_single(nccl_out, nsend, outs, ins)
+    torch.cuda.synchronize()
+    dist.barrier()
+    n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0.record(stream)
+    for _ in range(args.steps):
+        disp.route(args.seed)
+        disp.pack(tokens)
+        dist.all_to_all_single(nccl_out, nsend, outs, ins)
+    n1.record(stream)
+    torch.cuda.synchronize()
+    nms = torch.tensor([n0.elapsed_time(n1) / args.steps], device="cuda")
+    dist.all_reduce(nms, op=dist.ReduceOp.MAX)
+    nms = float(nms.item())
+    D = comm.demand().cpu().numpy()
+    cross = int(D.sum())
+    bn = int(max(D.sum(0).max(), D.sum(1).max()))
+    res = None
+    if rank == 0:
+        res = {"metric": "MoE dispatch throughput (gating -> histogram -> schedule -> pack -> "
+                         "alltoallv -> unpack; whole job)",
+               "value": round(T * world / (ms * 1e-3), 1), "unit": "tokens/s",
+               "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "bf16 payload (bytes moved as u8)",
+               "data": "synthetic tokens, deterministic integer top-2 gating",
+               "config": {"workload": "config3_moe_dispatch", "virtual_servers": f"{n}x{m}",
+                          "experts": world, "top_k": 2, "tokens_per_gpu": T,
+                          "hidden": hidden, "cross_gpu_bytes": cross,
+                          "bottleneck_gpu_bytes": bn},
+               "t_roof_us": round(bn / (PEER_GBS * 1e9) * 1e6, 1),
+               "frac_of_alltoallv_roofline": round(bn / (PEER_GBS * 1e9) / (ms * 1e-3), 4),
+               "nccl_path": {"ms": round(nms, 4),
+                             "value": round(T * world / (nms * 1e-3), 1), "unit": "tokens/s",
+                             "what": "same route+pack kernels + NCCL all_to_all_single"},
+               "clocks": clk.summary(),
+               "parity": "expert input == NCCL all_to_all_single of the packed buffer"}
+    comm.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    return res

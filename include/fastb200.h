@@ -119,11 +119,19 @@ int fast_decompose_batch(const int64_t *S, int B, int n, int mode,
 #define FAST_BUF_RECV 1
 #define FAST_BUF_STAGING 2
 
-/* One byte-range copy executed by `exec_rank` into `dst_rank`'s buffer. */
+/* One byte-range copy executed by `exec_rank` into `dst_rank`'s buffer,
+ * moved in chunks of the plan's chunk size.  Ops that land in a peer's
+ * staging own `nchunks(len)` flag slots there starting at sig_slot (each
+ * chunk publishes its slot with the call's epoch); ops that read staging
+ * wait for the producer chunks covering [wait_off, wait_off + len) of the
+ * producer op whose slots start at wait_slot (on the executing rank). */
 typedef struct {
   int64_t src_off;
   int64_t dst_off;
   int64_t len;
+  int64_t wait_off;
+  int32_t sig_slot;  /* -1: lands in recv (counted) */
+  int32_t wait_slot; /* -1: no dependency */
   int16_t exec_rank;
   int16_t dst_rank;
   uint8_t src_buf;
@@ -131,6 +139,9 @@ typedef struct {
   uint8_t phase;
   uint8_t stage; /* position in the ascending stage order */
 } fast_op;
+
+/* Flag slots per rank available to one plan (fast_comm flags region). */
+#define FAST_MAX_SLOTS 65536
 
 /* Compiled plan buffers (device pointers, caller-owned). */
 typedef struct {
@@ -153,8 +164,8 @@ int64_t fast_plan_op_capacity(int n, int m);
  * both sides); self bytes are never transferred. */
 int fast_plan_compile(const int64_t *D, const int64_t *send_self, int n, int m,
                       const fast_sched_bufs *sched, int64_t recv_capacity,
-                      int64_t staging_capacity, const fast_plan *plan,
-                      void *stream);
+                      int64_t staging_capacity, int64_t chunk_bytes,
+                      const fast_plan *plan, void *stream);
 
 /* Same plan logic on HOST pointers -- validation/inspection only (CPU
  * tests); the executor never calls it.  `order/perm/sbytes` are one
@@ -163,7 +174,8 @@ int fast_plan_compile_host(const int64_t *D, const int64_t *send_self, int n,
                            int m, int n_stages,
                            const int32_t *order, const uint8_t *perm,
                            const int64_t *sbytes, int64_t recv_capacity,
-                           int64_t staging_capacity, fast_op *ops,
+                           int64_t staging_capacity, int64_t chunk_bytes,
+                           fast_op *ops,
                            int64_t op_capacity, int32_t *n_ops,
                            int64_t *staging_used, void *workspace);
 
@@ -196,8 +208,10 @@ int fast_gather_demand(fast_comm *c, const int64_t *row, int64_t epoch,
                        void *stream);
 
 /* Execute a compiled plan: one persistent kernel per rank (`blocks` CTAs);
- * entry barrier, then balance pushes, intra copies and stage sends, then
- * redistribution, all chunked (`chunk_bytes`) and flag-synchronised.
+ * entry barrier, then producer CTAs run balance pushes, intra copies and
+ * stage sends while a byte-proportional set of CTAs forwards redistribution
+ * chunks as soon as their producer chunks have landed; chunk_bytes must be
+ * the plan's.
  * On return (stream order) the local recv buffer holds the alltoallv
  * result.  timeline_ns (device int64[8 + 2*256] or NULL) receives
  * %globaltimer stamps: [0] start, [1] barrier passed, [2] balance arrivals

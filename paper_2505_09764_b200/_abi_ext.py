@@ -16,8 +16,8 @@ SIGNATURES: list[tuple[str, object, list]] = [
     # executor: plan compile (exec.cu / plan.cuh)
     ("fast_plan_workspace_bytes", ctypes.c_size_t, [I, I]),
     ("fast_plan_op_capacity", I64, [I, I]),
-    ("fast_plan_compile", I, [V, V, I, I, P_SCHED, I64, I64, P_PLAN, V]),
-    ("fast_plan_compile_host", I, [V, V, I, I, I, V, V, V, I64, I64, V, I64, V, V, V]),
+    ("fast_plan_compile", I, [V, V, I, I, P_SCHED, I64, I64, I64, P_PLAN, V]),
+    ("fast_plan_compile_host", I, [V, V, I, I, I, V, V, V, I64, I64, I64, V, I64, V, V, V]),
     # communicator + P2P execution
     ("fast_comm_create", I, [I, I, I, I64, I64, ctypes.POINTER(V)]),
     ("fast_comm_ipc_handle", I, [V, V]),

@@ -32,14 +32,13 @@
 
 namespace {
 
-constexpr int64_t kFlagBytes = 4096;
+constexpr int64_t kCtrBytes = 4096;                                // counters
+constexpr int64_t kFlagBytes = kCtrBytes + (int64_t)FAST_MAX_SLOTS * 8;  // + slot flags
 constexpr int CTR_ARRIVE = 0;   // entry barrier, monotonic (+1 per peer/call)
 constexpr int CTR_GO = 1;       // local: barrier passed for epoch
-constexpr int CTR_BAL = 2;      // balance chunks landed in my staging
 constexpr int CTR_RECV = 3;     // chunks landed in my recv
 constexpr int CTR_GATHER = 4;   // demand rows landed (monotonic)
 constexpr int CTR_STATUS = 5;   // local error word
-constexpr int CTR_STAGE = 8;    // + k: stage-k chunks landed in my staging
 constexpr int kMaxStages = 256;
 constexpr int kExecThreads = 512;
 constexpr long long kSpinLimitNs = 20LL * 1000 * 1000 * 1000;  // 20 s
@@ -56,6 +55,9 @@ __device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
 }
 __device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void red_release_sys_add(uint64_t* p, uint64_t v) {
   asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -99,6 +101,9 @@ struct ExecArgs {
 
 __device__ __forceinline__ uint64_t* ctr(uint8_t* base, int idx) {
   return reinterpret_cast<uint64_t*>(base) + idx;
+}
+__device__ __forceinline__ uint64_t* slot_flag(uint8_t* base, int64_t slot) {
+  return reinterpret_cast<uint64_t*>(base + kCtrBytes) + slot;
 }
 
 // ---- CTA-wide byte copy, 16-byte vectorised on the destination ------------
@@ -208,7 +213,7 @@ __device__ __forceinline__ int64_t nchunks(int64_t len, int64_t chunk) {
 // for -- 1 in the multi-process mode, all `world` ranks in the one-GPU group
 // mode (cooperative launch, so every rank's CTAs are co-resident).
 __global__ void __launch_bounds__(kExecThreads) exec_kernel(ExecArgs a) {
-  __shared__ int64_t s_exp[3 + kMaxStages];  // bal, recv, (unused), stage k
+  __shared__ unsigned long long s_red[3];  // recv chunks expected, producer / redist bytes
   __shared__ int s_fail;
   a.rank += blockIdx.y;
   a.send = a.sends[blockIdx.y];
@@ -216,81 +221,92 @@ __global__ void __launch_bounds__(kExecThreads) exec_kernel(ExecArgs a) {
   uint8_t* me = a.peers[a.rank];
   uint64_t* status = ctr(me, CTR_STATUS);
   const int tid = threadIdx.x;
+  const uint64_t epoch = (uint64_t)a.epoch;
   if (tid == 0) s_fail = 0;
 
-  // ---- entry barrier (CTA 0): reset own counters, then arrive everywhere --
+  // ---- entry barrier (CTA 0): reset the recv counter, arrive everywhere ---
   if (blockIdx.x == 0 && tid == 0) {
     if (a.timeline) a.timeline[0] = (int64_t)globaltimer();
-    volatile uint64_t* c = reinterpret_cast<volatile uint64_t*>(me);
-    c[CTR_BAL] = 0;
-    c[CTR_RECV] = 0;
-    for (int k = 0; k < kMaxStages; ++k) c[CTR_STAGE + k] = 0;
+    reinterpret_cast<volatile uint64_t*>(me)[CTR_RECV] = 0;
     __threadfence_system();
     for (int r = 0; r < a.world; ++r)
       if (r != a.rank) red_release_sys_add(ctr(a.peers[r], CTR_ARRIVE), 1);
-    if (!wait_geq(ctr(me, CTR_ARRIVE), (uint64_t)a.epoch * (a.world - 1), true)) s_fail = 1;
-    st_release_gpu(ctr(me, CTR_GO), (uint64_t)a.epoch);
+    if (!wait_geq(ctr(me, CTR_ARRIVE), epoch * (a.world - 1), true)) s_fail = 1;
+    st_release_gpu(ctr(me, CTR_GO), epoch);
     if (a.timeline) a.timeline[1] = (int64_t)globaltimer();
   } else if (tid == 0) {
-    if (!wait_geq(ctr(me, CTR_GO), (uint64_t)a.epoch, false)) s_fail = 1;
+    if (!wait_geq(ctr(me, CTR_GO), epoch, false)) s_fail = 1;
   }
-  // expected arrivals into this rank, from the global op list
-  for (int i = tid; i < 3 + kMaxStages; i += blockDim.x) s_exp[i] = 0;
+  if (tid < 3) s_red[tid] = 0ull;
   __syncthreads();
   const int nops = (*a.plan_status == FAST_OK) ? *a.n_ops : 0;
-  for (int i = tid; i < nops; i += blockDim.x) {
-    const fast_op o = a.ops[i];
-    if (o.dst_rank != a.rank) continue;
-    const int64_t nc = nchunks(o.len, a.chunk);
-    if (o.dst_buf == FAST_BUF_RECV) atomicAdd((unsigned long long*)&s_exp[1], (unsigned long long)nc);
-    else if (o.phase == FAST_PH_BALANCE) atomicAdd((unsigned long long*)&s_exp[0], (unsigned long long)nc);
-    else atomicAdd((unsigned long long*)&s_exp[3 + o.stage], (unsigned long long)nc);
+  {
+    unsigned long long rc = 0, pb = 0, rb = 0;
+    for (int i = tid; i < nops; i += blockDim.x) {
+      const fast_op o = a.ops[i];
+      if (o.dst_rank == a.rank && o.dst_buf == FAST_BUF_RECV) rc += nchunks(o.len, a.chunk);
+      if (o.exec_rank == a.rank) {
+        if (o.phase == FAST_PH_REDIST) rb += o.len;
+        else pb += o.len;
+      }
+    }
+    if (rc) atomicAdd(&s_red[0], rc);
+    if (pb) atomicAdd(&s_red[1], pb);
+    if (rb) atomicAdd(&s_red[2], rb);
   }
   __syncthreads();
+  // CTA pools: producers (balance, intra, stage sends) and forwarders
+  // (redistribution), sized by bytes; producers never wait on forwarders.
+  const int NB = gridDim.x;
+  int R = 0;
+  if (s_red[2] > 0 && NB > 1) {
+    R = (int)((double)NB * (double)s_red[2] / (double)(s_red[1] + s_red[2]) + 0.5);
+    R = R < 1 ? 1 : (R > NB - 1 ? NB - 1 : R);
+  }
+  const bool fwd = (int)blockIdx.x >= NB - R;
+  const int pool = R == 0 ? NB : (fwd ? R : NB - R);
+  const int idx = fwd ? (int)blockIdx.x - (NB - R) : (int)blockIdx.x;
 
-  // ---- my ops, phase-ordered, chunks dealt round-robin over CTAs ----------
   int64_t item = 0;
-  bool bal_ready = false;
   for (int i = 0; i < nops && !s_fail; ++i) {
     const fast_op o = a.ops[i];
     if (o.exec_rank != a.rank) continue;
+    if (R > 0 && ((o.phase == FAST_PH_REDIST) != fwd)) continue;
     const int64_t nc = nchunks(o.len, a.chunk);
-    int64_t c = ((int64_t)blockIdx.x - item) % gridDim.x;
-    if (c < 0) c += gridDim.x;
+    int64_t c = ((int64_t)idx - item) % pool;
+    if (c < 0) c += pool;
     item += nc;
     if (c >= nc) continue;
-    // wait for this op's inputs (once per op per CTA)
-    if (o.phase == FAST_PH_FROM_STAGING && !bal_ready) {
-      if (tid == 0 && !wait_geq(ctr(me, CTR_BAL), (uint64_t)s_exp[0], true)) s_fail = 1;
-      bal_ready = true;
-      if (blockIdx.x == 0 && tid == 0 && a.timeline) a.timeline[2] = (int64_t)globaltimer();
-    } else if (o.phase == FAST_PH_REDIST) {
-      if (tid == 0 && !wait_geq(ctr(me, CTR_STAGE + o.stage), (uint64_t)s_exp[3 + o.stage], true))
-        s_fail = 1;
-    }
-    __syncthreads();
-    if (s_fail) break;
     const uint8_t* src = (o.src_buf == FAST_BUF_SEND ? a.send : me + a.staging_off) + o.src_off;
     uint8_t* peer = a.peers[o.dst_rank];
     uint8_t* dst = peer + (o.dst_buf == FAST_BUF_RECV ? a.recv_off : a.staging_off) + o.dst_off;
-    uint64_t* sig = ctr(peer, o.dst_buf == FAST_BUF_RECV ? CTR_RECV
-                              : o.phase == FAST_PH_BALANCE ? CTR_BAL : CTR_STAGE + o.stage);
     const bool nc_ok = o.src_buf == FAST_BUF_SEND;
-    for (; c < nc; c += gridDim.x) {
+    for (; c < nc; c += pool) {
       const int64_t off = c * a.chunk;
       const int64_t len = o.len - off < a.chunk ? o.len - off : a.chunk;
+      if (o.wait_slot >= 0) {  // producer chunks covering this chunk's source bytes
+        if (tid == 0) {
+          const int64_t p0 = (o.wait_off + off) / a.chunk;
+          const int64_t p1 = (o.wait_off + off + len - 1) / a.chunk;
+          for (int64_t q = p0; q <= p1 && !s_fail; ++q)
+            if (!wait_geq(slot_flag(me, o.wait_slot + q), epoch, true)) s_fail = 1;
+        }
+        __syncthreads();
+        if (s_fail) break;
+      }
       cta_copy(dst + off, src + off, len, nc_ok);
       __syncthreads();
       if (tid == 0) {
         __threadfence_system();
-        red_release_sys_add(sig, 1);
+        if (o.sig_slot >= 0) st_release_sys(slot_flag(peer, o.sig_slot + c), epoch);
+        else red_release_sys_add(ctr(peer, CTR_RECV), 1);
       }
     }
   }
   __syncthreads();
   if (blockIdx.x == 0 && tid == 0) {
     if (a.timeline) a.timeline[3] = (int64_t)globaltimer();
-    if (!s_fail && !wait_geq(ctr(me, CTR_RECV), (uint64_t)s_exp[1], true)) s_fail = 1;
+    if (!s_fail && !wait_geq(ctr(me, CTR_RECV), (uint64_t)s_red[0], true)) s_fail = 1;
     if (a.timeline) a.timeline[4] = (int64_t)globaltimer();
   }
   __syncthreads();
@@ -335,7 +351,8 @@ int64_t fast_plan_op_capacity(int n, int m) {
 
 int fast_plan_compile(const int64_t* D, const int64_t* send_self, int n, int m,
                       const fast_sched_bufs* sched, int64_t recv_capacity,
-                      int64_t staging_capacity, const fast_plan* plan, void* stream) {
+                      int64_t staging_capacity, int64_t chunk_bytes, const fast_plan* plan,
+                      void* stream) {
   if (!sched || !plan || n < 2 || m < 1 || m > FAST_MAX_GPUS_PER_SERVER) return FAST_EVALIDATION;
   fastplan::PlanIn in;
   in.n = n;
@@ -350,6 +367,7 @@ int fast_plan_compile(const int64_t* D, const int64_t* send_self, int n, int m,
   in.recv_cap = recv_capacity;
   in.staging_cap = staging_capacity;
   in.op_cap = plan->op_capacity;
+  in.chunk = chunk_bytes & ~(int64_t)15;
   fastplan::PlanOut out;
   out.ops = plan->ops;
   out.n_ops = plan->n_ops;
@@ -364,7 +382,8 @@ int fast_plan_compile(const int64_t* D, const int64_t* send_self, int n, int m,
 int fast_plan_compile_host(const int64_t* D, const int64_t* send_self, int n, int m,
                            int n_stages, const int32_t* order,
                            const uint8_t* perm, const int64_t* sbytes, int64_t recv_capacity,
-                           int64_t staging_capacity, fast_op* ops, int64_t op_capacity,
+                           int64_t staging_capacity, int64_t chunk_bytes, fast_op* ops,
+                           int64_t op_capacity,
                            int32_t* n_ops, int64_t* staging_used, void* workspace) {
   if (n < 2 || m < 1 || m > FAST_MAX_GPUS_PER_SERVER || !D || !ops || !workspace)
     return FAST_EVALIDATION;
@@ -381,6 +400,7 @@ int fast_plan_compile_host(const int64_t* D, const int64_t* send_self, int n, in
   in.recv_cap = recv_capacity;
   in.staging_cap = staging_capacity;
   in.op_cap = op_capacity;
+  in.chunk = chunk_bytes & ~(int64_t)15;
   int32_t status = 0;
   fastplan::PlanOut out;
   out.ops = ops;
@@ -403,7 +423,7 @@ int fast_comm_create(int rank, int world, int max_gpus_per_row, int64_t recv_byt
   c->world = world;
   c->recv_bytes = recv_bytes;
   c->staging_bytes = staging_bytes;
-  c->demand_off = kFlagBytes;
+  c->demand_off = kFlagBytes;  // counters + per-chunk slot flags
   c->recv_off = fastplan::align16(c->demand_off + 2 * ((int64_t)world * world + world) * 8 + 256);
   c->recv_off = (c->recv_off + 4095) & ~(int64_t)4095;
   c->staging_off = (c->recv_off + recv_bytes + 64 + 4095) & ~(int64_t)4095;

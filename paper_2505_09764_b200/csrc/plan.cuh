@@ -37,7 +37,7 @@ struct Take {
   int64_t seg_off;  // offset inside the giver's segment for (j, q)
   int64_t stg_off;  // where it lands in the taker's staging
   int32_t g, h, q;  // local giver, taker, column
-  int32_t pad;
+  int32_t slot;     // first flag slot of its balance op on the taker
 };
 
 FAST_HD inline int64_t align16(int64_t x) { return (x + 15) & ~(int64_t)15; }
@@ -55,6 +55,7 @@ FAST_HD inline int64_t plan_ws_bytes(int n, int m) {
   b += (int64_t)n * n * 8;               // delivered per pair
   b += T * m * 3 * 8;                    // lane cursors (cell q, piece, offset)
   b += G * 8;                            // staging top per rank
+  b += G * 8;                            // flag-slot top per rank
   b += (int64_t)m * m * 8 + 64;          // tile scratch
   return align16(b);
 }
@@ -77,6 +78,7 @@ struct PlanIn {
   const int64_t* sbytes;     // [K][n]
   int64_t recv_cap, staging_cap;
   int64_t op_cap;
+  int64_t chunk;             // exec chunk size (flag granularity)
 };
 
 struct PlanOut {
@@ -96,6 +98,7 @@ struct Ws {
   int64_t* delivered;
   int64_t* cursor;  // [T][m][3]: q, piece index within cell, offset in piece
   int64_t* stg_top;
+  int64_t* slot_top;
   int64_t* tbuf;  // [m][m] tile scratch
 };
 
@@ -112,6 +115,7 @@ FAST_HD inline Ws carve(void* p, int n, int m) {
   w.delivered = (int64_t*)c; c += (int64_t)n * n * 8;
   w.cursor = (int64_t*)c; c += T * m * 3 * 8;
   w.stg_top = (int64_t*)c; c += G * 8;
+  w.slot_top = (int64_t*)c; c += G * 8;
   w.tbuf = (int64_t*)c;
   return w;
 }
@@ -138,6 +142,9 @@ FAST_HD inline fast_op make_op(int phase, int stage, int exec_rank, int src_buf,
   o.src_off = src_off;
   o.dst_off = dst_off;
   o.len = len;
+  o.wait_off = 0;
+  o.sig_slot = -1;
+  o.wait_slot = -1;
   o.exec_rank = (int16_t)exec_rank;
   o.dst_rank = (int16_t)dst_rank;
   o.src_buf = (uint8_t)src_buf;
@@ -189,7 +196,7 @@ FAST_HD inline int replay_balance(int64_t* t /*m*m, modified*/, int m, Take* tak
       tk.g = g;
       tk.h = h;
       tk.q = q;
-      tk.pad = 0;
+      tk.slot = -1;
       takes[nt++] = tk;
     }
     dev[g] -= chunk;
@@ -202,7 +209,8 @@ FAST_HD inline int replay_balance(int64_t* t /*m*m, modified*/, int m, Take* tak
 // part (length orig_len), pieces 1.. are takes with h == p, q == q in order.
 FAST_HD inline bool cell_piece(const Ws& w, int tix, int m, int p, int q, int64_t piece,
                                int64_t* len, int* origin, int64_t* seg_off, int* in_staging,
-                               int64_t* loc_off) {
+                               int64_t* loc_off, int* slot) {
+  *slot = -1;
   if (piece == 0) {
     *len = w.orig_len[(int64_t)tix * m * m + p * m + q];
     *origin = p;
@@ -221,6 +229,7 @@ FAST_HD inline bool cell_piece(const Ws& w, int tix, int m, int p, int q, int64_
         *seg_off = tk[a].seg_off;
         *in_staging = 1;
         *loc_off = tk[a].stg_off;
+        *slot = tk[a].slot;
         return true;
       }
     }
@@ -262,7 +271,14 @@ FAST_HD inline void plan_compile(const PlanIn& in, const PlanOut& out) {
     }
     if (a > in.recv_cap) status = FAST_EVALIDATION;
   }
-  for (int r = 0; r < G; ++r) w.stg_top[r] = 0;
+  for (int r = 0; r < G; ++r) w.stg_top[r] = 0, w.slot_top[r] = 0;
+  const int64_t CH = in.chunk > 0 ? in.chunk : ((int64_t)1 << 20);
+  // flag slots of an op that lands in `rank`'s staging (one per chunk)
+  auto take_slots = [&](int rank, int64_t len) -> int32_t {
+    const int64_t s0 = w.slot_top[rank];
+    w.slot_top[rank] = s0 + (len + CH - 1) / CH;
+    return (int32_t)s0;
+  };
   for (int c = 0; c < n * n; ++c) w.delivered[c] = 0;
 
   // ---- phase 0: balancing pushes (into the taker's staging) ---------------
@@ -287,9 +303,12 @@ FAST_HD inline void plan_compile(const PlanIn& in, const PlanOut& out) {
         w.orig_len[(int64_t)tix * m * m + tk[a].g * m + tk[a].q] = tk[a].seg_off;
         tk[a].stg_off = w.stg_top[hi];
         w.stg_top[hi] = align16(w.stg_top[hi] + tk[a].x);
-        sk.push(0, make_op(FAST_PH_BALANCE, 0, gi, FAST_BUF_SEND,
-                           w.send_off[(int64_t)gi * G + dst] + tk[a].seg_off, hi,
-                           FAST_BUF_STAGING, tk[a].stg_off, tk[a].x));
+        tk[a].slot = take_slots(hi, tk[a].x);
+        fast_op o = make_op(FAST_PH_BALANCE, 0, gi, FAST_BUF_SEND,
+                            w.send_off[(int64_t)gi * G + dst] + tk[a].seg_off, hi,
+                            FAST_BUF_STAGING, tk[a].stg_off, tk[a].x);
+        o.sig_slot = tk[a].slot;
+        sk.push(0, o);
       }
       for (int c = 0; c < m * 3; ++c) w.cursor[(int64_t)tix * m * 3 + c] = 0;
     }
@@ -307,55 +326,79 @@ FAST_HD inline void plan_compile(const PlanIn& in, const PlanOut& out) {
       }
 
   // ---- stage windows + redistribution --------------------------------------
+  // Within a stage, sends that land in a proxy's staging (and must be
+  // forwarded) are emitted before sends that land in their final buffer, so
+  // proxies can start forwarding early; bucket 1 = own bytes, 2 = balanced-in
+  // bytes (waits for their balance chunks), 3 = redistribution.
   for (int s = 0; s < in.n_stages && status == FAST_OK; ++s) {
     const int k = in.order[s];
-    for (int i = 0; i < n && status == FAST_OK; ++i) {
-      const int64_t b = in.sbytes[(int64_t)k * n + i];
-      if (b <= 0) continue;
-      const int j = in.perm[(int64_t)k * n + i];
-      const int tix = tile_index(n, i, j);
-      const int64_t c0 = w.delivered[i * n + j], c1 = c0 + b;
-      w.delivered[i * n + j] = c1;
-      for (int p = 0; p < m; ++p) {
-        int64_t want = (c1 + m - 1 - p) / m - (c0 + m - 1 - p) / m;
-        int64_t* cur = w.cursor + ((int64_t)tix * m + p) * 3;  // q, piece, off
-        const int src_rank = i * m + p, proxy = j * m + p;
-        while (want > 0) {
-          if (cur[0] >= m) { status = FAST_EINVARIANT; break; }
-          int64_t len, seg_off, loc_off;
-          int origin, in_stg;
-          if (!cell_piece(w, tix, m, p, (int)cur[0], cur[1], &len, &origin, &seg_off,
-                          &in_stg, &loc_off)) {
-            cur[0] += 1;  // next cell of the lane stream
-            cur[1] = 0;
-            cur[2] = 0;
-            continue;
+    for (int pass = 0; pass < 2 && status == FAST_OK; ++pass) {
+      for (int i = 0; i < n && status == FAST_OK; ++i) {
+        const int64_t b = in.sbytes[(int64_t)k * n + i];
+        if (b <= 0) continue;
+        const int j = in.perm[(int64_t)k * n + i];
+        const int tix = tile_index(n, i, j);
+        const int64_t c0 = w.delivered[i * n + j];
+        const int64_t c1 = c0 + b;
+        for (int p = 0; p < m; ++p) {
+          int64_t want = (c1 + m - 1 - p) / m - (c0 + m - 1 - p) / m;
+          int64_t* cur = w.cursor + ((int64_t)tix * m + p) * 3;  // q, piece, off
+          int64_t cq = cur[0], cpc = cur[1], coff = cur[2];       // pass-local walk
+          const int src_rank = i * m + p, proxy = j * m + p;
+          while (want > 0) {
+            if (cq >= m) { status = FAST_EINVARIANT; break; }
+            int64_t len, seg_off, loc_off;
+            int origin, in_stg, slot;
+            if (!cell_piece(w, tix, m, p, (int)cq, cpc, &len, &origin, &seg_off, &in_stg,
+                            &loc_off, &slot)) {
+              cq += 1;  // next cell of the lane stream
+              cpc = 0;
+              coff = 0;
+              continue;
+            }
+            const int64_t avail = len - coff;
+            if (avail <= 0) { cpc += 1; coff = 0; continue; }
+            const int64_t x = want < avail ? want : avail;
+            const int q = (int)cq;
+            const bool staged = q != p;
+            if (staged == (pass == 0)) {
+              const int fin = j * m + q, orig = i * m + origin;
+              const int64_t src_off = in_stg ? loc_off + coff
+                                             : w.send_off[(int64_t)src_rank * G + fin] + coff;
+              const int64_t fin_off = w.recv_off[(int64_t)orig * G + fin] + seg_off + coff;
+              const int bucket = in_stg ? 2 : 1;
+              const int ph = in_stg ? FAST_PH_FROM_STAGING : FAST_PH_DIRECT;
+              const int sbuf = in_stg ? FAST_BUF_STAGING : FAST_BUF_SEND;
+              fast_op o;
+              if (!staged) {
+                o = make_op(ph, s, src_rank, sbuf, src_off, proxy, FAST_BUF_RECV, fin_off, x);
+              } else {
+                const int64_t stg = w.stg_top[proxy];
+                w.stg_top[proxy] = align16(stg + x);
+                o = make_op(ph, s, src_rank, sbuf, src_off, proxy, FAST_BUF_STAGING, stg, x);
+                o.sig_slot = take_slots(proxy, x);
+                fast_op r = make_op(FAST_PH_REDIST, s, proxy, FAST_BUF_STAGING, stg, fin,
+                                    FAST_BUF_RECV, fin_off, x);
+                r.wait_slot = o.sig_slot;
+                r.wait_off = 0;
+                sk.push(3, r);
+              }
+              if (in_stg) {
+                o.wait_slot = slot;  // the balance op that brought these bytes
+                o.wait_off = coff;
+              }
+              sk.push(bucket, o);
+            }
+            coff += x;
+            want -= x;
           }
-          const int64_t avail = len - cur[2];
-          if (avail <= 0) { cur[1] += 1; cur[2] = 0; continue; }
-          const int64_t x = want < avail ? want : avail;
-          const int q = (int)cur[0];
-          const int fin = j * m + q, orig = i * m + origin;
-          const int64_t src_off = in_stg ? loc_off + cur[2]
-                                         : w.send_off[(int64_t)src_rank * G + fin] + cur[2];
-          const int64_t fin_off = w.recv_off[(int64_t)orig * G + fin] + seg_off + cur[2];
-          const int bucket = in_stg ? 2 : 1;
-          const int ph = in_stg ? FAST_PH_FROM_STAGING : FAST_PH_DIRECT;
-          const int sbuf = in_stg ? FAST_BUF_STAGING : FAST_BUF_SEND;
-          if (q == p) {
-            sk.push(bucket, make_op(ph, s, src_rank, sbuf, src_off, proxy, FAST_BUF_RECV,
-                                    fin_off, x));
-          } else {
-            const int64_t stg = w.stg_top[proxy];
-            w.stg_top[proxy] = align16(stg + x);
-            sk.push(bucket, make_op(ph, s, src_rank, sbuf, src_off, proxy, FAST_BUF_STAGING,
-                                    stg, x));
-            sk.push(3, make_op(FAST_PH_REDIST, s, proxy, FAST_BUF_STAGING, stg, fin,
-                               FAST_BUF_RECV, fin_off, x));
+          if (pass == 1) {  // commit the walk after the second pass
+            cur[0] = cq;
+            cur[1] = cpc;
+            cur[2] = coff;
           }
-          cur[2] += x;
-          want -= x;
         }
+        if (pass == 1) w.delivered[i * n + j] = c1;
       }
     }
   }
@@ -371,6 +414,7 @@ FAST_HD inline void plan_compile(const PlanIn& in, const PlanOut& out) {
   for (int r = 0; r < G; ++r) {
     out.staging_used[r] = w.stg_top[r];
     if (w.stg_top[r] > in.staging_cap && status == FAST_OK) status = FAST_EVALIDATION;
+    if (w.slot_top[r] > FAST_MAX_SLOTS && status == FAST_OK) status = FAST_EVALIDATION;
   }
   if (sk.overflow && status == FAST_OK) status = FAST_EINVARIANT;
   // compact the buckets: [balance][direct][from staging][redistribution]

@@ -30,6 +30,7 @@ from .model import Topology, ValidationError, validate_topology
 from .synth import SynthBuffers, _device, _stream_handle
 
 OP_DTYPE = np.dtype([("src_off", "<i8"), ("dst_off", "<i8"), ("len", "<i8"),
+                     ("wait_off", "<i8"), ("sig_slot", "<i4"), ("wait_slot", "<i4"),
                      ("exec_rank", "<i2"), ("dst_rank", "<i2"), ("src_buf", "u1"),
                      ("dst_buf", "u1"), ("phase", "u1"), ("stage", "u1")])
 PH_BALANCE, PH_DIRECT, PH_FROM_STAGING, PH_REDIST = 0, 1, 2, 3
@@ -94,7 +95,7 @@ class PlanBuffers:
 
 def plan_compile_host(D: np.ndarray, n: int, m: int, order: np.ndarray, perm: np.ndarray,
                       sbytes: np.ndarray, recv_cap: int, staging_cap: int,
-                      send_self: np.ndarray | None = None):
+                      send_self: np.ndarray | None = None, chunk: int = DEFAULT_CHUNK):
     """Host build of the plan logic (validation / inspection only)."""
     lib = _lib.load()
     D = np.ascontiguousarray(D, dtype=np.int64)
@@ -113,7 +114,8 @@ def plan_compile_host(D: np.ndarray, n: int, m: int, order: np.ndarray, perm: np
     ss = None if send_self is None else np.ascontiguousarray(send_self, dtype=np.int64)
     st = lib.fast_plan_compile_host(p(D), None if ss is None else p(ss), n, m,
                                     int(order.shape[0]), p(order), p(perm_k),
-                                    p(sb_k), int(recv_cap), int(staging_cap), p(ops), cap,
+                                    p(sb_k), int(recv_cap), int(staging_cap), int(chunk),
+                                    p(ops), cap,
                                     p(n_ops), p(used), p(ws))
     return ops[: int(n_ops[0])].copy(), used, int(st)
 
@@ -216,7 +218,8 @@ class FastComm:
         sself = ctypes.c_void_p(dptr + 8 * self.world * self.world)
         _lib.check_rc(lib.fast_plan_compile(ctypes.c_void_p(dptr), sself, n, m,
                                             ctypes.byref(self.sched.struct), self.recv_bytes,
-                                            self.staging_bytes, ctypes.byref(self.plan.struct), sh),
+                                            self.staging_bytes, self.chunk,
+                                            ctypes.byref(self.plan.struct), sh),
                       "fast_plan_compile")
         tl = ctypes.c_void_p(self.timeline.data_ptr()) if record_timeline else None
         if exec_events is not None:
@@ -345,7 +348,7 @@ class GroupComm:
                       "fast_synth_batch")
         sp_self = None if self._self is None else ctypes.c_void_p(self._self.data_ptr())
         _lib.check_rc(lib.fast_plan_compile(dp, sp_self, n, m, ctypes.byref(self.sched.struct),
-                                            self.recv_bytes, self.staging_bytes,
+                                            self.recv_bytes, self.staging_bytes, self.chunk,
                                             ctypes.byref(self.plan.struct), sh),
                       "fast_plan_compile")
         sp = (ctypes.c_void_p * self.world)(*[s.data_ptr() for s in sends])

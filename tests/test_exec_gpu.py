@@ -83,7 +83,7 @@ def test_device_plan_equals_host_plan():
     out = oracle.synthesize_batch(D, n, m)
     p = PackedSchedule(**oracle.packed_fields(out, 0, n, m))
     host_ops, used, st = plan_compile_host(D, n, m, p.stage_order, p.stage_perm, p.stage_bytes,
-                                           comm.recv_bytes, comm.staging_bytes)
+                                           comm.recv_bytes, comm.staging_bytes, chunk=comm.chunk)
     assert st == 0
     assert dev_ops.dtype == OP_DTYPE
     assert np.array_equal(dev_ops, host_ops)

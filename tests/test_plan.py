@@ -37,7 +37,34 @@ def replay(ops, sends, G, recv_cap, stg_cap):
     return recv
 
 
-def check_instance(D: np.ndarray, n: int, m: int):
+def check_flags(ops, chunk):
+    """Every staging consumer waits on exactly the producer chunks that write
+    its source bytes (the executor's per-chunk flag protocol)."""
+    producers = {}
+    for o in ops:
+        if o["sig_slot"] >= 0:
+            assert o["dst_buf"] == BUF_STAGING
+            producers[(int(o["dst_rank"]), int(o["sig_slot"]))] = o
+        else:
+            assert o["dst_buf"] == BUF_RECV
+    slots = defaultdict(set)
+    for (r, s0), o in producers.items():
+        nch = (int(o["len"]) + chunk - 1) // chunk
+        for c in range(nch):
+            assert (s0 + c) not in slots[r], "flag slots overlap"
+            slots[r].add(s0 + c)
+    for o in ops:
+        if o["src_buf"] == BUF_STAGING:
+            assert o["wait_slot"] >= 0
+            prod = producers[(int(o["exec_rank"]), int(o["wait_slot"]))]
+            lo = int(prod["dst_off"]) + int(o["wait_off"])
+            assert int(o["src_off"]) == lo
+            assert int(o["wait_off"]) + int(o["len"]) <= int(prod["len"])
+        else:
+            assert o["wait_slot"] < 0
+
+
+def check_instance(D: np.ndarray, n: int, m: int, chunk: int = 4096):
     G = n * m
     out = oracle.synthesize_batch(D, n, m)
     assert int(out["status"][0]) == 0
@@ -45,8 +72,9 @@ def check_instance(D: np.ndarray, n: int, m: int):
     recv_cap = int(D.sum(axis=0).max()) + 16
     stg_cap = int(D.sum()) + 16 * G * G * 4 + 1024
     ops, used, st = plan_compile_host(D, n, m, p.stage_order, p.stage_perm, p.stage_bytes,
-                                      recv_cap, stg_cap)
+                                      recv_cap, stg_cap, chunk=chunk)
     assert st == 0
+    check_flags(ops, chunk)
     assert (used <= stg_cap).all()
     # phase order
     assert np.all(np.diff(ops["phase"].astype(int)) >= 0)
