@@ -31,9 +31,7 @@ namespace {
 
 constexpr int kBalThreads = 256;
 constexpr int kDecWarps = 4;  // matrices per CTA in decompose_kernel
-#ifndef FAST_DFS_ALL_LANES
-#define FAST_DFS_ALL_LANES 0
-#endif
+
 constexpr int64_t kMaxSafeTotal = int64_t(1) << 62;  // model.py:26
 
 __device__ __forceinline__ int64_t sat_add(int64_t s, int64_t v) {
@@ -287,8 +285,8 @@ struct DecSh {
   int16_t* newcol; // [n]
   int16_t* pick;   // [n]
   int16_t* freed;  // [n]
-  uint32_t* chg;   // [NWP] rows whose match changed
-  uint32_t* freeb; // [NWP] free columns (cm < 0)
+  uint32_t* chg;   // [NWP] rows whose match changed (bit r%32 of word r/32)
+  uint32_t* freeb; // [NWP] free columns (cm < 0), support-bitset layout
 };
 
 template <int NW>
@@ -297,7 +295,8 @@ __host__ __device__ __forceinline__ size_t dec_smem_bytes_t(int n) {
   size_t b = 2 * (size_t)n * NWP * 4;      // sup, supc
   b += 2 * (size_t)(n + 1) * 8;            // R, C
   b += 4 * (size_t)n * 2;                  // cm newcol pick freed
-  b += 2 * NWP * 4;                        // chg, freeb
+  b += NWP * 4 + 16;                       // chg
+  b += NWP * 4 + 16;                       // freeb
   return (b + 15) & ~(size_t)15;
 }
 
@@ -309,8 +308,8 @@ __device__ __forceinline__ DecSh<NW> dec_carve_t(char* p, int n) {
   s.supc = (uint32_t*)p; p += (size_t)n * NWP * 4;
   s.R = (int64_t*)p; p += (size_t)(n + 1) * 8;
   s.C = (int64_t*)p; p += (size_t)(n + 1) * 8;
-  s.chg = (uint32_t*)p; p += NWP * 4;
-  s.freeb = (uint32_t*)p; p += NWP * 4;
+  s.chg = (uint32_t*)p; p += NWP * 4 + 16;
+  s.freeb = (uint32_t*)p; p += NWP * 4 + 16;
   s.cm = (int16_t*)p; p += n * 2;
   s.newcol = (int16_t*)p; p += n * 2;
   s.pick = (int16_t*)p; p += n * 2;
@@ -318,108 +317,67 @@ __device__ __forceinline__ DecSh<NW> dec_carve_t(char* p, int n) {
   return s;
 }
 
-template <int NQ>
-__device__ __forceinline__ void load_row(const uint32_t* src, uint64_t (&row)[NQ]) {
-  if constexpr (NQ == 2) {
-    const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(src);
-    row[0] = x.x;
-    row[1] = x.y;
-  } else {
-    row[0] = *reinterpret_cast<const uint64_t*>(src);
-  }
-}
-
-// Kuhn augment(root) with a fresh `seen` (birkhoff.py:172-180).
-// The reference scans v = 0..n-1 and descends into the first column with
-// work[u][v] > 0 that is not seen.  When a frame resumes after a failed
-// child, every support column left of the failed one is already seen, so
-// "first set bit of support & ~seen" is exactly the reference's next v; no
-// resume cursor is needed.  All 32 lanes run the search redundantly on
-// identical (broadcast) data, so the warp never diverges and the loop has no
-// reconvergence overhead.  Returns the depth of the successful path
-// (pick[k] = column taken at depth k, pick[depth] free) or -1.
-template <int NW>
-__device__ __forceinline__ int first_unseen(const uint32_t (&row)[2 * DecSh<NW>::NQ],
-                                            const uint32_t (&seen)[2 * DecSh<NW>::NQ]) {
-  constexpr int NWP = 2 * DecSh<NW>::NQ;
-  int best = 0x7fff;
-#pragma unroll
-  for (int w = 0; w < NWP; ++w) {
-    const uint32_t c = row[w] & ~seen[w];
-    const int f = c ? (w * 32 + __ffs(c) - 1) : 0x7fff;
-    best = f < best ? f : best;
-  }
-  return best;
-}
+// Column layout of the support bitsets: u64 word q holds columns 64q..64q+63
+// with column 64q + b at bit 63 - b, so "first column of row & ~seen" is a
+// count-leading-zeros per 64-bit half.  In the u32 view that is word
+// (v >> 5) ^ 1, bit 31 - (v & 31).
+__device__ __forceinline__ int colword(int v) { return (v >> 5) ^ 1; }
+__device__ __forceinline__ uint32_t colbit(int v) { return 0x80000000u >> (v & 31); }
 
 template <int NW>
-__device__ __forceinline__ void load_row32(const uint32_t* src, uint32_t (&row)[2 * DecSh<NW>::NQ]) {
+__device__ __forceinline__ void load_row64(const uint32_t* src, uint64_t& r0, uint64_t& r1) {
   if constexpr (DecSh<NW>::NQ == 2) {
-    const uint4 x = *reinterpret_cast<const uint4*>(src);
-    row[0] = x.x; row[1] = x.y; row[2] = x.z; row[3] = x.w;
+    const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(src);
+    r0 = x.x;
+    r1 = x.y;
   } else {
-    const uint2 x = *reinterpret_cast<const uint2*>(src);
-    row[0] = x.x; row[1] = x.y;
+    r0 = *reinterpret_cast<const uint64_t*>(src);
+    r1 = 0ull;
   }
 }
 
+// Kuhn augment(root) with a fresh `seen` (birkhoff.py:172-180), one thread.
+// When a frame resumes after a failed child every support column left of
+// the failed one is already seen, so "first column of support & ~seen" is
+// exactly the reference's next v and no resume cursor is needed.  Returns
+// the depth of the successful path (pick[k] = column taken at depth k,
+// pick[depth] free) or -1.
 template <int NW>
-__device__ int dfs_search(const DecSh<NW>& s, const int root,
-                          const uint32_t (&freew)[2 * DecSh<NW>::NQ]) {
-  constexpr int NQ = DecSh<NW>::NQ;
+__device__ int dfs_search(const DecSh<NW>& s, const int root, uint64_t free0,
+                          uint64_t free1) {
   constexpr int NWP = DecSh<NW>::NWP;
-  uint64_t freeq[NQ], seen[NQ], row[NQ];
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    freeq[q] = (uint64_t)freew[2 * q] | ((uint64_t)freew[2 * q + 1] << 32);
-    seen[q] = 0ull;
-  }
-  load_row<NQ>(s.sup + root * NWP, row);
+  uint64_t seen0 = 0ull, seen1 = 0ull, r0, r1;
+  load_row64<NW>(s.sup + root * NWP, r0, r1);
   int sp = 0;
   for (;;) {
-    const uint64_t c0 = row[0] & ~seen[0];
-    int v;
-    if constexpr (NQ == 2) {
-      const uint64_t c1 = row[1] & ~seen[1];
-      v = c0 ? __ffsll(c0) - 1 : (c1 ? 63 + __ffsll(c1) : -1);
-    } else {
-      v = c0 ? __ffsll(c0) - 1 : -1;
-    }
-    if (v < 0) {
+    const uint64_t c0 = r0 & ~seen0, c1 = r1 & ~seen1;
+    const int v = c0 ? __clzll(c0) : (c1 ? 64 + __clzll(c1) : -1);
+    if (__builtin_expect(v < 0, 0)) {
       if (sp == 0) return -1;
       --sp;
-      load_row<NQ>(sp == 0 ? s.sup + root * NWP : s.supc + s.pick[sp - 1] * NWP, row);
+      load_row64<NW>(sp == 0 ? s.sup + root * NWP : s.supc + s.pick[sp - 1] * NWP, r0, r1);
       continue;
     }
-    const uint64_t bit = 1ull << (v & 63);
-    bool is_free;
-    if constexpr (NQ == 2) {
-      const bool hi = v >= 64;
-      seen[0] |= hi ? 0ull : bit;
-      seen[1] |= hi ? bit : 0ull;
-      is_free = ((hi ? freeq[1] : freeq[0]) & bit) != 0ull;
-    } else {
-      seen[0] |= bit;
-      is_free = (freeq[0] & bit) != 0ull;
-    }
+    const uint64_t m = 0x8000000000000000ull >> (v & 63);
+    const bool hi = v >= 64;
+    seen0 |= hi ? 0ull : m;
+    seen1 |= hi ? m : 0ull;
     s.pick[sp] = (int16_t)v;
-    if (is_free) return sp;
+    if (((hi ? free1 : free0) & m) != 0ull) return sp;
     ++sp;
-    load_row<NQ>(s.supc + v * NWP, row);
+    load_row64<NW>(s.supc + v * NWP, r0, r1);
   }
 }
 
 // Lane 0 searches, the result is broadcast (the other lanes wait).
 template <int NW>
-__device__ __forceinline__ int dfs_warp(const DecSh<NW>& s, const int root,
-                                        const uint32_t (&freew)[2 * DecSh<NW>::NQ]) {
-#if FAST_DFS_ALL_LANES
-  return dfs_search<NW>(s, root, freew);
-#else
+__device__ __forceinline__ int dfs_warp(const DecSh<NW>& s, const int root) {
   int depth = 0;
-  if ((threadIdx.x & 31) == 0) depth = dfs_search<NW>(s, root, freew);
+  if ((threadIdx.x & 31) == 0) {
+    const uint64_t* fq = reinterpret_cast<const uint64_t*>(s.freeb);
+    depth = dfs_search<NW>(s, root, fq[0], DecSh<NW>::NQ == 2 ? fq[1] : 0ull);
+  }
   return __shfl_sync(0xffffffffu, depth, 0);
-#endif
 }
 
 // Apply an augmenting path (warp-wide): cm[pick[k]] = row_k where row_0 =
@@ -446,6 +404,7 @@ __device__ __forceinline__ void apply_path(const DecSh<NW>& s, const int root,
 #pragma unroll
       for (int w = 0; w < NWP; ++w) s.supc[v * NWP + w] = s.sup[r * NWP + w];
       atomicOr(&s.chg[r >> 5], 1u << (r & 31));
+      if (k == depth) atomicAnd(&s.freeb[colword(v)], ~colbit(v));  // matched now
     }
   }
   __syncwarp();
@@ -544,9 +503,10 @@ __global__ void __launch_bounds__(kDecWarps * 32)
   for (int u = lane; u < n; u += 32) s.cm[u] = -1;
   if (lane < NWP) {
     s.chg[lane] = 0u;
-    const int lo = lane * 32;
-    s.freeb[lane] = lo >= n ? 0u : (n - lo >= 32 ? 0xffffffffu : ((1u << (n - lo)) - 1u));
+    s.freeb[lane] = 0u;
   }
+  __syncwarp();
+  for (int v = lane; v < n; v += 32) atomicOr(&s.freeb[colword(v)], colbit(v));
   __syncwarp();
   for (int u = 0; u < n; ++u) {
     const int64_t r0 = s.R[u], r1 = s.R[u + 1];
@@ -567,10 +527,10 @@ __global__ void __launch_bounds__(kDecWarps * 32)
         aux_out[(int64_t)u * n + v] = a;
         work[(int64_t)u * n + v] = e;
       }
-      const uint32_t bits = __ballot_sync(0xffffffffu, e > 0);
-      if (lane == 0) s.sup[u * NWP + w] = bits;
+      const uint32_t bits = __brev(__ballot_sync(0xffffffffu, e > 0));
+      if (lane == 0) s.sup[u * NWP + (w ^ 1)] = bits;
     }
-    if (NWP > NW && lane == 0) s.sup[u * NWP + NWP - 1] = 0u;
+    if (NWP > NW && lane == 0) s.sup[u * NWP + ((NWP - 1) ^ 1)] = 0u;
   }
   if (lane == 0) out.common_sum[b] = common;
   __syncwarp();
@@ -584,23 +544,15 @@ __global__ void __launch_bounds__(kDecWarps * 32)
   }
 
   // ---- initial Kuhn matching (birkhoff.py:182-186) -----------------------
-  uint32_t freew[NWP];
-#pragma unroll
-  for (int w = 0; w < NWP; ++w) freew[w] = s.freeb[w];
   for (int u = 0; u < n; ++u) {
-    const int depth = dfs_warp<NW>(s, u, freew);
+    const int depth = dfs_warp<NW>(s, u);
     if (depth < 0) { st = FAST_EINVARIANT; break; }
     apply_path<NW>(s, u, depth, lane);
-    const int vf = s.pick[depth];
-#pragma unroll
-    for (int w = 0; w < NWP; ++w)
-      if ((vf >> 5) == w) freew[w] &= ~(1u << (vf & 31));
   }
   if (st != FAST_OK) {
     if (lane == 0) { *status = st; out.n_raw[b] = 0; out.n_stages[b] = 0; }
     return;
   }
-  if (lane < NWP) s.freeb[lane] = 0u;  // perfect matching: no free column
   // lane-owned row state
   int rcol[NW];
   int64_t mv[NW], offv[NW];
@@ -651,7 +603,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
         pout[(int64_t)k * n + u] = (uint8_t)v;
         real_pos = real > 0;
         if (mv[r] == 0) {
-          s.sup[u * NWP + (v >> 5)] &= ~(1u << (v & 31));
+          s.sup[u * NWP + colword(v)] &= ~colbit(v);
           fr = remaining > 0;
         }
       }
@@ -664,7 +616,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
       if (fr) {
         s.freed[nfreed + __popc(fb & ((1u << lane) - 1u))] = (int16_t)u;
         s.cm[rcol[r]] = -1;  // unmatch (birkhoff.py:210-214)
-        atomicOr(&s.freeb[rcol[r] >> 5], 1u << (rcol[r] & 31));
+        atomicOr(&s.freeb[colword(rcol[r])], colbit(rcol[r]));
         rcol[r] = -1;
       }
       nfreed += __popc(fb);
@@ -682,25 +634,13 @@ __global__ void __launch_bounds__(kDecWarps * 32)
     if (remaining == 0) break;
     __syncwarp();
     // re-augment freed rows in index order (birkhoff.py:215-219)
-#pragma unroll
-    for (int w = 0; w < NWP; ++w) freew[w] = s.freeb[w];
     for (int f = 0; f < nfreed; ++f) {
       const int u = s.freed[f];
-      const int depth = dfs_warp<NW>(s, u, freew);
+      const int depth = dfs_warp<NW>(s, u);
       if (depth < 0) { st = FAST_EINVARIANT; break; }
       apply_path<NW>(s, u, depth, lane);
-      const int vf = s.pick[depth];
-#pragma unroll
-      for (int w = 0; w < NWP; ++w)
-        if ((vf >> 5) == w) freew[w] &= ~(1u << (vf & 31));
     }
     if (st != FAST_OK) break;
-    __syncwarp();
-    if (lane < NWP) {
-#pragma unroll
-      for (int w = 0; w < NWP; ++w)
-        if (lane == w) s.freeb[w] = freew[w];
-    }
     // rows whose cell changed: write the old (non-zero) value back, fetch
     // the new cell; all loads are issued before any is consumed.
     uint32_t chg[NW];
@@ -713,9 +653,9 @@ __global__ void __launch_bounds__(kDecWarps * 32)
 #pragma unroll
     for (int r = 0; r < NW; ++r) {
       const int u = r * 32 + lane;
-      moved[r] = u < n && ((chg[r] >> lane) & 1u);
+      const int nc = (u < n && ((chg[r] >> lane) & 1u)) ? s.newcol[u] : rcol[r];
+      moved[r] = nc != rcol[r];
       if (moved[r]) {
-        const int nc = s.newcol[u];
         if (rcol[r] >= 0) work[(int64_t)u * n + rcol[r]] = mv[r];
         rcol[r] = nc;
         nv[r] = work[(int64_t)u * n + nc];
