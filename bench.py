@@ -345,7 +345,9 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--workload", choices=("auto", "synth", "alltoallv", "moe"), default="auto")
+    ap.add_argument("--workload", choices=("auto", "synth", "alltoallv", "moe", "sweep"),
+                    default="auto")
+    ap.add_argument("--sweep-max", type=int, default=1 << 30)
     ap.add_argument("--n", type=int, default=128)
     ap.add_argument("--m", type=int, default=8)
     ap.add_argument("--batch", type=int, default=1000)
@@ -377,9 +379,14 @@ def main() -> None:
         print(json.dumps(res), flush=True)
         return
     from bench_exec import run as run_exec
-    from bench_exec import run_moe
+    from bench_exec import run_moe, run_sweep
 
-    res = run_moe(args) if workload == "moe" else run_exec(args, workload)
+    if workload == "moe":
+        res = run_moe(args)
+    elif workload == "sweep":
+        res = run_sweep(args)
+    else:
+        res = run_exec(args, workload)
     if res is not None:
         print(json.dumps(res), flush=True)
 

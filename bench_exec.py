@@ -354,3 +354,99 @@ def run_moe(args) -> dict | None:
     dist.barrier()
     dist.destroy_process_group()
     return res
+
+
+def run_sweep(args) -> dict | None:
+    """BASELINE config 4: per-step shifting hotspot (GPU k mod N is hot, its row
+    and column x8 over a uniform base), per-GPU send size swept 1 KiB -> 1 GiB
+    in x4 steps.  Every step has a new traffic matrix, so the demand
+    all-gather + synthesis + plan are on the critical path; reports the
+    end-to-end step time, the exec-kernel time and NCCL all_to_all_single."""
+    from paper_2505_09764_b200 import Topology, workloads
+    from paper_2505_09764_b200.executor import FastComm
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, m = topology_for(world, args.topo or ("4x2" if world == 8 else None))
+    t = Topology(n, m)
+    sizes = [1024 * 4 ** k for k in range(11) if 1024 * 4 ** k <= args.sweep_max]
+    steps = max(args.steps, world)  # every GPU is hot at least once
+    mats = {}
+    cap = stg = 0
+    for S in sizes:
+        ds = []
+        for it in range(steps):
+            mean = max(1, S // (world - 1) // 2)  # uniform base: mean row ~ S
+            d = workloads.gen_hotspot(1000 * it + 7, t, mean, hot=it % world, factor=8).sizes
+            ds.append(d)
+            cap = max(cap, int(d.sum(0).max()), int(d.sum(1).max()))
+        mats[S] = ds
+    cap += 4096
+    comm = FastComm(t, recv_bytes=cap, staging_bytes=2 * cap + (4 << 20), blocks=args.blocks,
+                    chunk_bytes=args.chunk)
+    send = torch.randint(0, 256, (cap,), dtype=torch.uint8, device="cuda")
+    nccl_out = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    rows_dev = {S: [torch.from_numpy(d[rank].copy()).cuda() for d in mats[S]] for S in sizes}
+    table = []
+    for S in sizes:
+        ds, rows = mats[S], rows_dev[S]
+        for it in range(min(args.warmup, steps)):
+            comm.alltoallv(send, rows[it])
+        torch.cuda.synchronize()
+        dist.barrier()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(steps)]
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for it in range(steps):
+            comm.alltoallv(send, rows[it], exec_events=ev[it])
+        t1.record(stream)
+        torch.cuda.synchronize()
+        comm.check()
+        fast_ms = t0.elapsed_time(t1) / steps
+        exec_ms = sum(a.elapsed_time(b) for a, b in ev) / steps
+        for it in range(min(args.warmup, steps)):
+            d = ds[it]
+            dist.all_to_all_single(nccl_out[: int(d[:, rank].sum())], send[: int(d[rank].sum())],
+                                   d[:, rank].tolist(), d[rank].tolist())
+        torch.cuda.synchronize()
+        dist.barrier()
+        n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n0.record(stream)
+        for it in range(steps):
+            d = ds[it]
+            dist.all_to_all_single(nccl_out[: int(d[:, rank].sum())], send[: int(d[rank].sum())],
+                                   d[:, rank].tolist(), d[rank].tolist())
+        n1.record(stream)
+        torch.cuda.synchronize()
+        nccl_ms = n0.elapsed_time(n1) / steps
+        v = torch.tensor([fast_ms, exec_ms, nccl_ms], device="cuda")
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        fast_ms, exec_ms, nccl_ms = (float(x) for x in v.tolist())
+        tot = sum(int(d.sum()) for d in ds) / steps
+        bn = sum(int(max(d.sum(0).max(), d.sum(1).max())) for d in ds) / steps
+        table.append({"bytes_per_gpu": S, "fast_us": round(fast_ms * 1e3, 2),
+                      "exec_us": round(exec_ms * 1e3, 2), "nccl_us": round(nccl_ms * 1e3, 2),
+                      "fast_GBps": round(tot / (fast_ms * 1e-3) / 1e9, 3),
+                      "nccl_GBps": round(tot / (nccl_ms * 1e-3) / 1e9, 3),
+                      "frac_roofline_exec": round(bn / (PEER_GBS * 1e9) / (exec_ms * 1e-3), 4)})
+    res = None
+    if rank == 0:
+        last = table[-1]
+        res = {"metric": "alltoallv algbw under a shifting hotspot (config 4; whole job, "
+                         "synthesis on the critical path every step)",
+               "value": last["fast_GBps"], "unit": "GB/s", "n_gpus": world, "steps": steps,
+               "warmup": args.warmup, "ms_per_step": round(last["fast_us"] / 1e3, 4),
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+               "data": "synthetic hotspot traffic (x8 row/col of GPU k mod N at step k)",
+               "config": {"workload": "config4_hotspot_sweep", "virtual_servers": f"{n}x{m}",
+                          "sizes": [r["bytes_per_gpu"] for r in table]},
+               "sweep": table}
+    comm.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    return res
