@@ -32,6 +32,17 @@ namespace {
 constexpr int kBalThreads = 256;
 constexpr int kDecWarps = 4;  // matrices per CTA in decompose_kernel
 
+// Optional section timers (debug builds with -DFAST_DEC_PROFILE only).
+#ifdef FAST_DEC_PROFILE
+__device__ unsigned long long g_dec_prof[8];
+#define DPROF_T(var) const long long var = clock64()
+#define DPROF_ADD(slot, val) \
+  if ((threadIdx.x & 31) == 0) atomicAdd(&g_dec_prof[slot], (unsigned long long)(val))
+#else
+#define DPROF_T(var)
+#define DPROF_ADD(slot, val)
+#endif
+
 constexpr int64_t kMaxSafeTotal = int64_t(1) << 62;  // model.py:26
 
 __device__ __forceinline__ int64_t sat_add(int64_t s, int64_t v) {
@@ -281,6 +292,10 @@ struct DecSh {
   uint32_t* supc;  // [n][NWP]
   int64_t* R;      // [n+1]
   int64_t* C;      // [n+1]
+  int64_t* auxl;   // [2n+2] aux_left of the NW-corner staircase cells
+  int16_t* alo;    // [n] first column of row u's staircase range
+  int16_t* ahi;    // [n] last column (alo - 1 when empty)
+  int16_t* aoff;   // [n] offset of row u's range in auxl
   int16_t* cm;     // [n]
   int16_t* newcol; // [n]
   int16_t* pick;   // [n]
@@ -294,6 +309,8 @@ __host__ __device__ __forceinline__ size_t dec_smem_bytes_t(int n) {
   constexpr int NWP = 2 * ((NW + 1) / 2);
   size_t b = 2 * (size_t)n * NWP * 4;      // sup, supc
   b += 2 * (size_t)(n + 1) * 8;            // R, C
+  b += (size_t)(2 * n + 2) * 8;            // auxl
+  b += 3 * (size_t)n * 2 + 16;             // alo ahi aoff
   b += 4 * (size_t)n * 2;                  // cm newcol pick freed
   b += NWP * 4 + 16;                       // chg
   b += NWP * 4 + 16;                       // freeb
@@ -308,12 +325,16 @@ __device__ __forceinline__ DecSh<NW> dec_carve_t(char* p, int n) {
   s.supc = (uint32_t*)p; p += (size_t)n * NWP * 4;
   s.R = (int64_t*)p; p += (size_t)(n + 1) * 8;
   s.C = (int64_t*)p; p += (size_t)(n + 1) * 8;
+  s.auxl = (int64_t*)p; p += (size_t)(2 * n + 2) * 8;
   s.chg = (uint32_t*)p; p += NWP * 4 + 16;
   s.freeb = (uint32_t*)p; p += NWP * 4 + 16;
   s.cm = (int16_t*)p; p += n * 2;
   s.newcol = (int16_t*)p; p += n * 2;
   s.pick = (int16_t*)p; p += n * 2;
-  s.freed = (int16_t*)p;
+  s.freed = (int16_t*)p; p += n * 2;
+  s.alo = (int16_t*)p; p += n * 2;
+  s.ahi = (int16_t*)p; p += n * 2;
+  s.aoff = (int16_t*)p;
   return s;
 }
 
@@ -342,6 +363,11 @@ __device__ __forceinline__ void load_row64(const uint32_t* src, uint64_t& r0, ui
 // exactly the reference's next v and no resume cursor is needed.  Returns
 // the depth of the successful path (pick[k] = column taken at depth k,
 // pick[depth] free) or -1.
+__device__ __forceinline__ int clz64(uint64_t x) {  // 64 for x == 0
+  const uint32_t hi = (uint32_t)(x >> 32), lo = (uint32_t)x;
+  return hi ? __clz(hi) : 32 + __clz(lo);
+}
+
 template <int NW>
 __device__ int dfs_search(const DecSh<NW>& s, const int root, uint64_t free0,
                           uint64_t free1) {
@@ -350,9 +376,11 @@ __device__ int dfs_search(const DecSh<NW>& s, const int root, uint64_t free0,
   load_row64<NW>(s.sup + root * NWP, r0, r1);
   int sp = 0;
   for (;;) {
-    const uint64_t c0 = r0 & ~seen0, c1 = r1 & ~seen1;
-    const int v = c0 ? __clzll(c0) : (c1 ? 64 + __clzll(c1) : -1);
-    if (__builtin_expect(v < 0, 0)) {
+    const int z0 = clz64(r0 & ~seen0), z1 = clz64(r1 & ~seen1);
+    const int v = z0 < 64 ? z0 : 64 + z1;  // 128: no unseen support column
+    uint64_t n0, n1;
+    load_row64<NW>(s.supc + (v & 127) * NWP, n0, n1);  // speculative next row
+    if (__builtin_expect(v == 128, 0)) {
       if (sp == 0) return -1;
       --sp;
       load_row64<NW>(sp == 0 ? s.sup + root * NWP : s.supc + s.pick[sp - 1] * NWP, r0, r1);
@@ -360,12 +388,14 @@ __device__ int dfs_search(const DecSh<NW>& s, const int root, uint64_t free0,
     }
     const uint64_t m = 0x8000000000000000ull >> (v & 63);
     const bool hi = v >= 64;
+    const uint64_t fm = (hi ? free1 : free0) & m;
     seen0 |= hi ? 0ull : m;
     seen1 |= hi ? m : 0ull;
     s.pick[sp] = (int16_t)v;
-    if (((hi ? free1 : free0) & m) != 0ull) return sp;
+    if (fm) return sp;
     ++sp;
-    load_row64<NW>(s.supc + v * NWP, r0, r1);
+    r0 = n0;
+    r1 = n1;
   }
 }
 
@@ -408,6 +438,12 @@ __device__ __forceinline__ void apply_path(const DecSh<NW>& s, const int root,
     }
   }
   __syncwarp();
+}
+
+// aux_left of cell (u, v): a slot of the row's staircase range, or -1.
+template <int NW>
+__device__ __forceinline__ int aux_slot(const DecSh<NW>& s, int u, int v) {
+  return (v >= s.alo[u] && v <= s.ahi[u]) ? s.aoff[u] + v - s.alo[u] : -1;
 }
 
 template <int NW>
@@ -532,7 +568,29 @@ __global__ void __launch_bounds__(kDecWarps * 32)
     }
     if (NWP > NW && lane == 0) s.sup[u * NWP + ((NWP - 1) ^ 1)] = 0u;
   }
-  if (lane == 0) out.common_sum[b] = common;
+  if (lane == 0) {
+    out.common_sum[b] = common;
+    // NW-corner staircase: row u's aux cells are the contiguous columns whose
+    // deficit interval overlaps [R_u, R_u+1); consecutive rows share at most
+    // one column, so all of them fit in 2n slots (aux_left lives here).
+    int v = 0, at = 0;
+    for (int u = 0; u < n; ++u) {
+      const int64_t r0 = s.R[u], r1 = s.R[u + 1];
+      if (mode != FAST_DEC_SERVER || r1 == r0) {
+        s.alo[u] = 0; s.ahi[u] = -1; s.aoff[u] = (int16_t)at;
+        continue;
+      }
+      while (v < n - 1 && s.C[v + 1] <= r0) ++v;
+      int e = v;
+      while (e < n - 1 && s.C[e + 1] < r1) ++e;
+      s.alo[u] = (int16_t)v; s.ahi[u] = (int16_t)e; s.aoff[u] = (int16_t)at;
+      for (int c = v; c <= e; ++c) {
+        const int64_t lo = r0 > s.C[c] ? r0 : s.C[c];
+        const int64_t hi = r1 < s.C[c + 1] ? r1 : s.C[c + 1];
+        s.auxl[at++] = hi > lo ? hi - lo : 0;
+      }
+    }
+  }
   __syncwarp();
   if (common == 0) {
     if (lane == 0) {
@@ -555,18 +613,19 @@ __global__ void __launch_bounds__(kDecWarps * 32)
   }
   // lane-owned row state
   int rcol[NW];
-  int64_t mv[NW], offv[NW];
+  int64_t mv[NW], am[NW];
 #pragma unroll
   for (int r = 0; r < NW; ++r) {
     const int u = r * 32 + lane;
     rcol[r] = -1;
     mv[r] = INT64_MAX;
-    offv[r] = 0;
+    am[r] = 0;
     if (u < n) {
       const int v = s.newcol[u];
       rcol[r] = v;
       mv[r] = work[(int64_t)u * n + v];
-      offv[r] = (mode == FAST_DEC_SERVER && u == v) ? 0 : S[(int64_t)u * n + v];
+      const int sl = aux_slot<NW>(s, u, v);
+      am[r] = sl >= 0 ? s.auxl[sl] : 0;
     }
   }
   if (lane < NWP) s.chg[lane] = 0u;
@@ -579,6 +638,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
   uint8_t* pout = out.stage_perm + (int64_t)b * K * n;
   int64_t* bout = out.stage_bytes + (int64_t)b * K * n;
   while (remaining > 0) {
+    DPROF_T(t0);
     if (k >= K) { st = FAST_EINVARIANT; break; }
     int64_t wl = INT64_MAX;
 #pragma unroll
@@ -594,11 +654,11 @@ __global__ void __launch_bounds__(kDecWarps * 32)
       const int vsave = rcol[r];
       if (u < n) {
         const int v = rcol[r];
-        const int64_t before = mv[r];
-        const int64_t spare = before - offv[r];
-        const int64_t charged = spare <= 0 ? 0 : (spare < weight ? spare : weight);
+        // strip_auxiliary (birkhoff.py:225-252): the cell pays aux first
+        const int64_t charged = am[r] < weight ? am[r] : weight;
         const int64_t real = weight - charged;
-        mv[r] = before - weight;
+        am[r] -= charged;
+        mv[r] -= weight;
         __stcs(bout + (int64_t)k * n + u, real);
         pout[(int64_t)k * n + u] = (uint8_t)v;
         real_pos = real > 0;
@@ -633,14 +693,23 @@ __global__ void __launch_bounds__(kDecWarps * 32)
     ++k;
     if (remaining == 0) break;
     __syncwarp();
+    DPROF_T(t1);
+    DPROF_ADD(0, t1 - t0);
     // re-augment freed rows in index order (birkhoff.py:215-219)
     for (int f = 0; f < nfreed; ++f) {
       const int u = s.freed[f];
+      DPROF_T(ta);
       const int depth = dfs_warp<NW>(s, u);
+      DPROF_T(tb);
       if (depth < 0) { st = FAST_EINVARIANT; break; }
       apply_path<NW>(s, u, depth, lane);
+      DPROF_T(tc);
+      DPROF_ADD(1, tb - ta);
+      DPROF_ADD(2, tc - tb);
+      DPROF_ADD(4, depth + 1);
     }
     if (st != FAST_OK) break;
+    DPROF_T(t2);
     // rows whose cell changed: write the old (non-zero) value back, fetch
     // the new cell; all loads are issued before any is consumed.
     uint32_t chg[NW];
@@ -648,7 +717,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
     for (int w = 0; w < NW; ++w) chg[w] = s.chg[w];
     __syncwarp();
     if (lane < NWP) s.chg[lane] = 0u;
-    int64_t nv[NW], no[NW];
+    int64_t nv[NW];
     bool moved[NW];
 #pragma unroll
     for (int r = 0; r < NW; ++r) {
@@ -656,20 +725,24 @@ __global__ void __launch_bounds__(kDecWarps * 32)
       const int nc = (u < n && ((chg[r] >> lane) & 1u)) ? s.newcol[u] : rcol[r];
       moved[r] = nc != rcol[r];
       if (moved[r]) {
-        if (rcol[r] >= 0) work[(int64_t)u * n + rcol[r]] = mv[r];
+        if (rcol[r] >= 0) {
+          work[(int64_t)u * n + rcol[r]] = mv[r];
+          const int so = aux_slot<NW>(s, u, rcol[r]);
+          if (so >= 0) s.auxl[so] = am[r];
+        }
         rcol[r] = nc;
         nv[r] = work[(int64_t)u * n + nc];
-        no[r] = S[(int64_t)u * n + nc];
+        const int sn = aux_slot<NW>(s, u, nc);
+        am[r] = sn >= 0 ? s.auxl[sn] : 0;
       }
     }
 #pragma unroll
-    for (int r = 0; r < NW; ++r) {
-      if (moved[r]) {
-        mv[r] = nv[r];
-        offv[r] = (mode == FAST_DEC_SERVER && r * 32 + lane == rcol[r]) ? 0 : no[r];
-      }
-    }
+    for (int r = 0; r < NW; ++r)
+      if (moved[r]) mv[r] = nv[r];
     __syncwarp();
+    DPROF_T(t3);
+    DPROF_ADD(3, t3 - t2);
+    DPROF_ADD(5, 1);
   }
 
   // ---- final invariants (birkhoff.py:216-221, :273-277): every cell peeled
@@ -829,6 +902,19 @@ bool bad_shape(int B, int n, int m) {
 }  // namespace
 
 extern "C" {
+
+#ifdef FAST_DEC_PROFILE
+int fast_debug_dec_prof(unsigned long long* out8, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out8, g_dec_prof, 8 * sizeof(unsigned long long)) != cudaSuccess)
+    return FAST_ECUDA;
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_dec_prof, z, sizeof(z));
+  }
+  return FAST_OK;
+}
+#endif
 
 int fast_version(void) { return 100; }
 
