@@ -230,6 +230,15 @@ int fast_comm_create_group(int world, int64_t recv_bytes, int64_t staging_bytes,
 int fast_exec_group(fast_comm *const *comms, int world, const fast_plan *plan,
                     const void *const *sends, int64_t epoch, int blocks,
                     int64_t chunk_bytes, int64_t *timeline_ns, void *stream);
+/* Base of `rank`'s symmetric block as mapped in this process (own block for
+ * rank == own rank); NULL before fast_comm_open_peers. */
+void *fast_comm_peer_ptr(const fast_comm *c, int rank);
+
+/* Diagnostics: the executor's CTA copy loop on raw pointers (either side
+ * may be a peer mapping) -- NVLink push/pull characterisation only. */
+int fast_debug_copy(void *dst, const void *src, int64_t bytes, int blocks,
+                    int64_t chunk, int nc, void *stream);
+
 /* Device status word of the last exec on this comm (0 ok, 3 = a wait timed
  * out: peers missing or protocol error). */
 int fast_comm_status(const fast_comm *c, int32_t *status_host);

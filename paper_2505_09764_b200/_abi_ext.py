@@ -31,6 +31,8 @@ SIGNATURES: list[tuple[str, object, list]] = [
     ("fast_gather_demand", I, [V, V, I64, V]),
     ("fast_exec", I, [V, P_PLAN, V, I64, I, I64, V, V]),
     ("fast_comm_status", I, [V, ctypes.POINTER(ctypes.c_int32)]),
+    ("fast_comm_peer_ptr", V, [V, I]),
+    ("fast_debug_copy", I, [V, V, I64, I, I64, I, V]),
     ("fast_comm_create_group", I, [I, I64, I64, ctypes.POINTER(V)]),
     ("fast_exec_group", I, [ctypes.POINTER(V), I, P_PLAN, ctypes.POINTER(V), I64, I, I64, V, V]),
     # MoE front-end (moe.cu)

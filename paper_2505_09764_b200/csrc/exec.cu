@@ -39,8 +39,13 @@ constexpr int CTR_GO = 1;       // local: barrier passed for epoch
 constexpr int CTR_RECV = 3;     // chunks landed in my recv
 constexpr int CTR_GATHER = 4;   // demand rows landed (monotonic)
 constexpr int CTR_STATUS = 5;   // local error word
+constexpr int CTR_WORK_P = 6;   // local: next producer chunk (reset per call)
+constexpr int CTR_WORK_F = 7;   // local: next forwarder chunk (reset per call)
 constexpr int kMaxStages = 256;
-constexpr int kExecThreads = 512;
+#ifndef FAST_EXEC_THREADS
+#define FAST_EXEC_THREADS 512
+#endif
+constexpr int kExecThreads = FAST_EXEC_THREADS;
 constexpr long long kSpinLimitNs = 20LL * 1000 * 1000 * 1000;  // 20 s
 
 __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
@@ -82,6 +87,9 @@ __device__ bool wait_geq(const uint64_t* p, uint64_t target, bool sys) {
   }
 }
 
+#ifndef FAST_COPY_UNROLL
+#define FAST_COPY_UNROLL 4  // 16-byte vectors in flight per thread per copy loop
+#endif
 constexpr int kMaxRanks = 16;       // one NVSwitch node
 constexpr int kTimelineStride = 8 + kMaxStages;
 
@@ -150,7 +158,7 @@ __device__ void cta_copy(uint8_t* dst, const uint8_t* src, int64_t len, bool nc)
   len -= head;
   const int64_t nw = len >> 4;
   const int sh = (int)((uintptr_t)src & 15);
-  constexpr int U = 4;
+  constexpr int U = FAST_COPY_UNROLL;
   if (sh == 0) {
     int64_t wi = tid;
     for (; wi + (U - 1) * nt < nw; wi += U * nt) {
@@ -209,6 +217,20 @@ __device__ __forceinline__ int64_t nchunks(int64_t len, int64_t chunk) {
   return (len + chunk - 1) / chunk;
 }
 
+// Raw CTA copy of `bytes` split over the grid (NVLink characterisation:
+// dst or src may be a peer mapping).  nc: read the source through the
+// non-coherent path.
+__global__ void __launch_bounds__(kExecThreads) raw_copy_kernel(uint8_t* dst, const uint8_t* src,
+                                                                int64_t bytes, int64_t chunk,
+                                                                int nc) {
+  const int64_t nch = (bytes + chunk - 1) / chunk;
+  for (int64_t c = blockIdx.x; c < nch; c += gridDim.x) {
+    const int64_t off = c * chunk;
+    const int64_t len = bytes - off < chunk ? bytes - off : chunk;
+    cta_copy(dst + off, src + off, len, nc != 0);
+  }
+}
+
 // grid (blocks, ranks_in_launch): blockIdx.y selects the rank this CTA acts
 // for -- 1 in the multi-process mode, all `world` ranks in the one-GPU group
 // mode (cooperative launch, so every rank's CTAs are co-resident).
@@ -228,6 +250,8 @@ __global__ void __launch_bounds__(kExecThreads) exec_kernel(ExecArgs a) {
   if (blockIdx.x == 0 && tid == 0) {
     if (a.timeline) a.timeline[0] = (int64_t)globaltimer();
     reinterpret_cast<volatile uint64_t*>(me)[CTR_RECV] = 0;
+    reinterpret_cast<volatile uint64_t*>(me)[CTR_WORK_P] = 0;
+    reinterpret_cast<volatile uint64_t*>(me)[CTR_WORK_F] = 0;
     __threadfence_system();
     for (int r = 0; r < a.world; ++r)
       if (r != a.rank) red_release_sys_add(ctr(a.peers[r], CTR_ARRIVE), 1);
@@ -264,43 +288,57 @@ __global__ void __launch_bounds__(kExecThreads) exec_kernel(ExecArgs a) {
     R = R < 1 ? 1 : (R > NB - 1 ? NB - 1 : R);
   }
   const bool fwd = (int)blockIdx.x >= NB - R;
-  const int pool = R == 0 ? NB : (fwd ? R : NB - R);
-  const int idx = fwd ? (int)blockIdx.x - (NB - R) : (int)blockIdx.x;
 
-  int64_t item = 0;
-  for (int i = 0; i < nops && !s_fail; ++i) {
+  // Dynamic chunk scheduling: each pool hands out its chunks in op-list
+  // (phase) order through a local atomic counter, so every chunk a CTA waits
+  // on was handed out earlier -- the same deadlock argument as a static
+  // deal -- while fast CTAs absorb the tail.
+  __shared__ long long s_item;
+  unsigned long long* wctr =
+      reinterpret_cast<unsigned long long*>(ctr(me, fwd ? CTR_WORK_F : CTR_WORK_P));
+  int i = 0;          // op cursor (monotone: grabbed items only increase)
+  int64_t base = 0;   // first item index of op i within this pool
+  for (;;) {
+    if (tid == 0) s_item = s_fail ? -1 : (long long)atomicAdd(wctr, 1ull);
+    __syncthreads();
+    const long long it = s_item;
+    __syncthreads();
+    if (it < 0) break;
+    // advance to the op holding item `it`
+    int64_t nc = 0;
+    bool found = false;
+    for (; i < nops; ++i) {
+      const fast_op& q = a.ops[i];
+      if (q.exec_rank != a.rank) continue;
+      if (R > 0 && ((q.phase == FAST_PH_REDIST) != fwd)) continue;
+      nc = nchunks(q.len, a.chunk);
+      if (it < base + nc) { found = true; break; }
+      base += nc;
+    }
+    if (!found) break;
     const fast_op o = a.ops[i];
-    if (o.exec_rank != a.rank) continue;
-    if (R > 0 && ((o.phase == FAST_PH_REDIST) != fwd)) continue;
-    const int64_t nc = nchunks(o.len, a.chunk);
-    int64_t c = ((int64_t)idx - item) % pool;
-    if (c < 0) c += pool;
-    item += nc;
-    if (c >= nc) continue;
+    const int64_t c = it - base;
     const uint8_t* src = (o.src_buf == FAST_BUF_SEND ? a.send : me + a.staging_off) + o.src_off;
     uint8_t* peer = a.peers[o.dst_rank];
     uint8_t* dst = peer + (o.dst_buf == FAST_BUF_RECV ? a.recv_off : a.staging_off) + o.dst_off;
-    const bool nc_ok = o.src_buf == FAST_BUF_SEND;
-    for (; c < nc; c += pool) {
-      const int64_t off = c * a.chunk;
-      const int64_t len = o.len - off < a.chunk ? o.len - off : a.chunk;
-      if (o.wait_slot >= 0) {  // producer chunks covering this chunk's source bytes
-        if (tid == 0) {
-          const int64_t p0 = (o.wait_off + off) / a.chunk;
-          const int64_t p1 = (o.wait_off + off + len - 1) / a.chunk;
-          for (int64_t q = p0; q <= p1 && !s_fail; ++q)
-            if (!wait_geq(slot_flag(me, o.wait_slot + q), epoch, true)) s_fail = 1;
-        }
-        __syncthreads();
-        if (s_fail) break;
-      }
-      cta_copy(dst + off, src + off, len, nc_ok);
-      __syncthreads();
+    const int64_t off = c * a.chunk;
+    const int64_t len = o.len - off < a.chunk ? o.len - off : a.chunk;
+    if (o.wait_slot >= 0) {  // producer chunks covering this chunk's source bytes
       if (tid == 0) {
-        __threadfence_system();
-        if (o.sig_slot >= 0) st_release_sys(slot_flag(peer, o.sig_slot + c), epoch);
-        else red_release_sys_add(ctr(peer, CTR_RECV), 1);
+        const int64_t p0 = (o.wait_off + off) / a.chunk;
+        const int64_t p1 = (o.wait_off + off + len - 1) / a.chunk;
+        for (int64_t q = p0; q <= p1 && !s_fail; ++q)
+          if (!wait_geq(slot_flag(me, o.wait_slot + q), epoch, true)) s_fail = 1;
       }
+      __syncthreads();
+      if (s_fail) break;
+    }
+    cta_copy(dst + off, src + off, len, o.src_buf == FAST_BUF_SEND);
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence_system();
+      if (o.sig_slot >= 0) st_release_sys(slot_flag(peer, o.sig_slot + c), epoch);
+      else red_release_sys_add(ctr(peer, CTR_RECV), 1);
     }
   }
   __syncthreads();
@@ -584,6 +622,19 @@ int fast_exec_group(fast_comm* const* comms, int world, const fast_plan* plan,
                                               dim3(kExecThreads), args, 0,
                                               (cudaStream_t)stream);
   return e == cudaSuccess ? FAST_OK : FAST_ECUDA;
+}
+
+void* fast_comm_peer_ptr(const fast_comm* c, int rank) {
+  if (!c || rank < 0 || rank >= c->world || !c->opened) return nullptr;
+  return c->peers_host[rank];
+}
+
+int fast_debug_copy(void* dst, const void* src, int64_t bytes, int blocks, int64_t chunk,
+                    int nc, void* stream) {
+  if (!dst || !src || bytes < 0 || blocks < 1 || chunk < 16) return FAST_EVALIDATION;
+  raw_copy_kernel<<<blocks, kExecThreads, 0, (cudaStream_t)stream>>>(
+      (uint8_t*)dst, (const uint8_t*)src, bytes, chunk & ~(int64_t)15, nc);
+  return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
 }
 
 int fast_comm_status(const fast_comm* c, int32_t* status_host) {
