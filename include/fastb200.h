@@ -230,6 +230,22 @@ int fast_comm_create_group(int world, int64_t recv_bytes, int64_t staging_bytes,
 int fast_exec_group(fast_comm *const *comms, int world, const fast_plan *plan,
                     const void *const *sends, int64_t epoch, int blocks,
                     int64_t chunk_bytes, int64_t *timeline_ns, void *stream);
+/* One FAST alltoallv, everything enqueued on `stream` (no host sync):
+ * demand all-gather of `counts` (device int64[world], entry `rank` = own
+ * segment kept in place), synthesis into `sched` (B = 1), plan compile into
+ * `plan`, P2P execution.  The receive buffer (fast_comm_recv_ptr) then holds
+ * the all_to_all_single layout with a gap at the self slot.  Replaces the
+ * paper's all_to_all_FAST runtime call. */
+int fast_alltoallv(fast_comm *c, const void *send, const int64_t *counts, int n,
+                   int m, const fast_sched_bufs *sched, const fast_plan *plan,
+                   int blocks, int64_t chunk_bytes, int64_t *timeline_ns,
+                   void *stream);
+/* Number of calls issued through fast_alltoallv (the current epoch); callers
+ * that drive fast_gather_demand / fast_exec themselves report theirs with
+ * fast_comm_set_epoch so both paths share one monotone counter. */
+int64_t fast_comm_epoch(const fast_comm *c);
+int fast_comm_set_epoch(fast_comm *c, int64_t epoch);
+
 /* Base of `rank`'s symmetric block as mapped in this process (own block for
  * rank == own rank); NULL before fast_comm_open_peers. */
 void *fast_comm_peer_ptr(const fast_comm *c, int rank);

@@ -352,16 +352,65 @@ __global__ void __launch_bounds__(kExecThreads) exec_kernel(ExecArgs a) {
 }
 
 // Device plan kernel: takes n_stages / synthesis status from device memory.
-__global__ void fast_plan_kernel_dev(fastplan::PlanIn in, fastplan::PlanOut out,
-                                     const int32_t* n_stages, const int32_t* sched_status) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// The plan is a sequential walk (one thread), so every input it touches and
+// its workspace are first staged into shared memory by the whole CTA when
+// they fit (`smem_ok`); otherwise it runs on the global copies.
+constexpr int kPlanThreads = 256;
+constexpr size_t kPlanSmemMax = 160 * 1024;
+
+__host__ __device__ inline size_t plan_smem_bytes(int n, int m) {
+  const int64_t G = (int64_t)n * m, K = (int64_t)n * n - 2 * n + 2;
+  size_t b = (size_t)fastplan::plan_ws_bytes(n, m) + 16;
+  b += (size_t)fastplan::plan_op_capacity(n, m, (int)K) * sizeof(fast_op);  // op buckets
+  b += (size_t)(G * G + G) * 8;        // D + self sizes
+  b += (size_t)K * 4 + 16;             // order
+  b += (size_t)K * n + 16;             // perm
+  b += (size_t)K * n * 8 + 16;         // stage bytes
+  return (b + 127) & ~(size_t)127;
+}
+
+__global__ void __launch_bounds__(kPlanThreads)
+    fast_plan_kernel_dev(fastplan::PlanIn in, fastplan::PlanOut out, const int32_t* n_stages,
+                         const int32_t* sched_status, int smem_ok) {
+  extern __shared__ __align__(16) char psm[];
   if (*sched_status != FAST_OK) {
-    *out.n_ops = 0;
-    *out.status = *sched_status;
+    if (threadIdx.x == 0) {
+      *out.n_ops = 0;
+      *out.status = *sched_status;
+    }
     return;
   }
   in.n_stages = *n_stages;
-  fastplan::plan_compile(in, out);
+  if (smem_ok) {
+    const int n = in.n, G = in.n * in.m, K = in.K;
+    char* p = psm;
+    char* ws = p; p += ((size_t)fastplan::plan_ws_bytes(in.n, in.m) + 16 + 15) & ~(size_t)15;
+    fast_op* scratch = (fast_op*)p; p += (size_t)in.op_cap * sizeof(fast_op);
+    int64_t* D = (int64_t*)p; p += (size_t)G * G * 8;
+    int64_t* ss = (int64_t*)p; p += (size_t)G * 8;
+    int32_t* ord = (int32_t*)p; p += ((size_t)K * 4 + 16 + 15) & ~(size_t)15;
+    int64_t* sb = (int64_t*)p; p += (size_t)K * n * 8 + 16;
+    uint8_t* pm = (uint8_t*)p;
+    for (int i = threadIdx.x; i < G * G; i += blockDim.x) D[i] = in.D[i];
+    for (int i = threadIdx.x; i < G; i += blockDim.x) ss[i] = in.send_self ? in.send_self[i] : 0;
+    for (int i = threadIdx.x; i < in.n_stages; i += blockDim.x) ord[i] = in.order[i];
+    // only the kept stages' rows are read by the plan; copy them compactly
+    // (row k of the raw arrays -> row k, K rows at most)
+    for (int i = threadIdx.x; i < in.n_stages * n; i += blockDim.x) {
+      const int k = in.order[i / n], u = i % n;
+      sb[(int64_t)k * n + u] = in.sbytes[(int64_t)k * n + u];
+      pm[(int64_t)k * n + u] = in.perm[(int64_t)k * n + u];
+    }
+    __syncthreads();
+    in.D = D;
+    in.send_self = in.send_self ? ss : nullptr;
+    in.order = ord;
+    in.sbytes = sb;
+    in.perm = pm;
+    out.ws = ws;
+    out.scratch = scratch;
+  }
+  if (threadIdx.x == 0) fastplan::plan_compile(in, out);
 }
 
 }  // namespace
@@ -375,6 +424,7 @@ struct fast_comm {
   uint8_t** peers_dev;       // [world] device copy
   cudaIpcMemHandle_t handle;
   int opened;
+  int64_t epoch;  // calls issued through fast_alltoallv
 };
 
 extern "C" {
@@ -412,8 +462,15 @@ int fast_plan_compile(const int64_t* D, const int64_t* send_self, int n, int m,
   out.staging_used = plan->staging_used;
   out.status = plan->status;
   out.ws = plan->workspace;
-  fast_plan_kernel_dev<<<1, 32, 0, (cudaStream_t)stream>>>(in, out, sched->n_stages,
-                                                           sched->status);
+  out.scratch = nullptr;
+  const size_t smem = plan_smem_bytes(n, m);
+  const int smem_ok = smem <= kPlanSmemMax;
+  if (smem_ok && cudaFuncSetAttribute(fast_plan_kernel_dev,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem) != cudaSuccess)
+    return FAST_ECUDA;
+  fast_plan_kernel_dev<<<1, kPlanThreads, smem_ok ? smem : 0, (cudaStream_t)stream>>>(
+      in, out, sched->n_stages, sched->status, smem_ok);
   return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
 }
 
@@ -446,6 +503,7 @@ int fast_plan_compile_host(const int64_t* D, const int64_t* send_self, int n, in
   out.staging_used = staging_used;
   out.status = &status;
   out.ws = workspace;
+  out.scratch = nullptr;
   fastplan::plan_compile(in, out);
   return status;
 }
@@ -635,6 +693,32 @@ int fast_debug_copy(void* dst, const void* src, int64_t bytes, int blocks, int64
   raw_copy_kernel<<<blocks, kExecThreads, 0, (cudaStream_t)stream>>>(
       (uint8_t*)dst, (const uint8_t*)src, bytes, chunk & ~(int64_t)15, nc);
   return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
+}
+
+int fast_alltoallv(fast_comm* c, const void* send, const int64_t* counts, int n, int m,
+                   const fast_sched_bufs* sched, const fast_plan* plan, int blocks,
+                   int64_t chunk_bytes, int64_t* timeline_ns, void* stream) {
+  if (!c || !c->opened || !send || !counts || !sched || !plan) return FAST_EVALIDATION;
+  if ((int64_t)n * m != c->world) return FAST_EVALIDATION;
+  const int64_t e = c->epoch + 1;
+  int rc = fast_gather_demand(c, counts, e, stream);
+  if (rc != FAST_OK) return rc;
+  c->epoch = e;
+  int64_t* D = fast_comm_demand_ptr(c, e);
+  rc = fast_synth_batch(D, 1, n, m, sched, stream);
+  if (rc != FAST_OK) return rc;
+  rc = fast_plan_compile(D, D + (int64_t)c->world * c->world, n, m, sched, c->recv_bytes,
+                         c->staging_bytes, chunk_bytes, plan, stream);
+  if (rc != FAST_OK) return rc;
+  return fast_exec(c, plan, send, e, blocks, chunk_bytes, timeline_ns, stream);
+}
+
+int64_t fast_comm_epoch(const fast_comm* c) { return c ? c->epoch : -1; }
+
+int fast_comm_set_epoch(fast_comm* c, int64_t epoch) {
+  if (!c || epoch < c->epoch) return FAST_EVALIDATION;
+  c->epoch = epoch;
+  return FAST_OK;
 }
 
 int fast_comm_status(const fast_comm* c, int32_t* status_host) {

@@ -83,6 +83,7 @@ struct PlanIn {
 
 struct PlanOut {
   fast_op* ops;              // [op_cap], phase-ordered
+  fast_op* scratch;          // [op_cap] bucket area (may alias ops)
   int32_t* n_ops;            // [1]
   int64_t* staging_used;     // [G]
   int32_t* status;           // [1]
@@ -243,7 +244,7 @@ FAST_HD inline void plan_compile(const PlanIn& in, const PlanOut& out) {
   const int T = n * (n - 1);
   Ws w = carve(out.ws, n, m);
   Sink sk;
-  sk.ops = out.ops;
+  sk.ops = out.scratch ? out.scratch : out.ops;
   sk.cap4 = in.op_cap / 4;
   sk.cnt[0] = sk.cnt[1] = sk.cnt[2] = sk.cnt[3] = 0;
   sk.overflow = false;
@@ -418,9 +419,12 @@ FAST_HD inline void plan_compile(const PlanIn& in, const PlanOut& out) {
   }
   if (sk.overflow && status == FAST_OK) status = FAST_EINVARIANT;
   // compact the buckets: [balance][direct][from staging][redistribution]
-  int64_t at = sk.cnt[0];
-  for (int bk = 1; bk < 4; ++bk)
-    for (int64_t x = 0; x < sk.cnt[bk]; ++x) out.ops[at++] = out.ops[bk * sk.cap4 + x];
+  int64_t at = 0;
+  for (int bk = 0; bk < 4; ++bk)
+    for (int64_t x = 0; x < sk.cnt[bk]; ++x) {
+      const fast_op o = sk.ops[bk * sk.cap4 + x];  // forward copy: at <= source index
+      out.ops[at++] = o;
+    }
   *out.n_ops = status == FAST_OK ? (int32_t)at : 0;
   *out.status = status;
   (void)T;

@@ -751,6 +751,26 @@ __global__ void __launch_bounds__(kDecWarps * 32)
     for (int c = lane; c < n * NWP; c += 32) left |= s.sup[c] != 0u;
     if (__any_sync(0xffffffffu, left)) st = FAST_EINVARIANT;
   }
+  // small stage capacity (n <= 6): sort_stages_ascending here with a warp
+  // bitonic network on (weight, src0|dst0|raw index) and skip sort_kernel
+  if (K <= 32 && st == FAST_OK && kept > 0) {
+    __syncwarp();
+    uint64_t w = lane < kept ? key_w[lane] : ~0ull;
+    uint32_t t = lane < kept ? key_t[lane] : ~0u;
+#pragma unroll
+    for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        const uint64_t w2 = __shfl_xor_sync(0xffffffffu, w, j);
+        const uint32_t t2 = __shfl_xor_sync(0xffffffffu, t, j);
+        const bool asc = (lane & kk) == 0;
+        const bool lower = (lane & j) == 0;
+        const bool gt = w > w2 || (w == w2 && t > t2);
+        if ((lower == asc) ? gt : !gt) { w = w2; t = t2; }
+      }
+    }
+    if (lane < kept) out.stage_order[(int64_t)b * K + lane] = (int32_t)(t & 0xffffu);
+  }
   if (lane == 0) {
     *status = st;
     out.n_raw[b] = k;
@@ -883,6 +903,7 @@ int launch_decompose(const int64_t* S, int B, int n, int mode, int check_total,
   if (cudaGetLastError() != cudaSuccess) return FAST_ECUDA;
   if (after_decompose && cudaEventRecord(after_decompose, s) != cudaSuccess)
     return FAST_ECUDA;
+  if (stage_cap(n) <= 32) return FAST_OK;  // sorted inside decompose_kernel
   const size_t ssmem = sort_smem_bytes(n);
   if (cudaFuncSetAttribute(sort_kernel,
                            cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -169,6 +169,8 @@ class FastComm:
         self.timeline = torch.zeros(TIMELINE_STRIDE, dtype=torch.int64, device=self.device)
         self.epoch = 0
         self.recv = bytes_view(lib.fast_comm_recv_ptr(ptr), self.recv_bytes, self.device)
+        self._sched_ref = ctypes.byref(self.sched.struct)
+        self._plan_ref = ctypes.byref(self.plan.struct)
 
     def close(self) -> None:
         if getattr(self, "_ptr", None):
@@ -206,10 +208,23 @@ class FastComm:
         if send.dtype != torch.uint8 or not send.is_cuda:
             raise ValidationError("send must be a cuda uint8 tensor")
         n, m = self.topology.n_servers, self.topology.gpus_per_server
-        row = send_counts.to(device=self.device, dtype=torch.int64).contiguous()
+        row = send_counts
+        if row.dtype != torch.int64 or row.device != self.device or not row.is_contiguous():
+            row = row.to(device=self.device, dtype=torch.int64).contiguous()
         self._row = row  # keep alive until the stream consumes it
+        s = stream or torch.cuda.current_stream()
+        tl = ctypes.c_void_p(self.timeline.data_ptr()) if record_timeline else None
+        if exec_events is None:
+            _lib.check_rc(lib.fast_alltoallv(self._ptr, ctypes.c_void_p(send.data_ptr()),
+                                             ctypes.c_void_p(row.data_ptr()), n, m,
+                                             self._sched_ref, self._plan_ref, self.blocks,
+                                             self.chunk, tl, ctypes.c_void_p(s.cuda_stream)),
+                          "fast_alltoallv")
+            self.epoch += 1
+            return self.recv
+        # step by step (exec-kernel events for the benchmark)
         self.epoch += 1
-        sh = _stream_handle(stream)
+        sh = ctypes.c_void_p(s.cuda_stream)
         _lib.check_rc(lib.fast_gather_demand(self._ptr, ctypes.c_void_p(row.data_ptr()),
                                              self.epoch, sh), "fast_gather_demand")
         dptr = lib.fast_comm_demand_ptr(self._ptr, self.epoch)
@@ -221,14 +236,12 @@ class FastComm:
                                             self.staging_bytes, self.chunk,
                                             ctypes.byref(self.plan.struct), sh),
                       "fast_plan_compile")
-        tl = ctypes.c_void_p(self.timeline.data_ptr()) if record_timeline else None
-        if exec_events is not None:
-            exec_events[0].record(stream or torch.cuda.current_stream())
+        exec_events[0].record(s)
         _lib.check_rc(lib.fast_exec(self._ptr, ctypes.byref(self.plan.struct),
                                     ctypes.c_void_p(send.data_ptr()), self.epoch, self.blocks,
                                     self.chunk, tl, sh), "fast_exec")
-        if exec_events is not None:
-            exec_events[1].record(stream or torch.cuda.current_stream())
+        exec_events[1].record(s)
+        _lib.check_rc(lib.fast_comm_set_epoch(self._ptr, self.epoch), "fast_comm_set_epoch")
         return self.recv
 
     def check(self) -> None:
