@@ -240,6 +240,11 @@ int fast_alltoallv(fast_comm *c, const void *send, const int64_t *counts, int n,
                    int m, const fast_sched_bufs *sched, const fast_plan *plan,
                    int blocks, int64_t chunk_bytes, int64_t *timeline_ns,
                    void *stream);
+/* fast_alltoallv runs gather + synthesis + plan inside the exec kernel's
+ * CTA 0 (one launch per call) when n <= 6 and this is enabled; the default
+ * is the multi-launch path (measured equal or faster on B200, see
+ * profiles/README.md). */
+int fast_comm_set_fused(fast_comm *c, int enable);
 /* Number of calls issued through fast_alltoallv (the current epoch); callers
  * that drive fast_gather_demand / fast_exec themselves report theirs with
  * fast_comm_set_epoch so both paths share one monotone counter. */

@@ -35,6 +35,7 @@ SIGNATURES: list[tuple[str, object, list]] = [
     ("fast_alltoallv", I, [V, V, V, I, I, P_SCHED, P_PLAN, I, I64, V, V]),
     ("fast_comm_epoch", I64, [V]),
     ("fast_comm_set_epoch", I, [V, I64]),
+    ("fast_comm_set_fused", I, [V, I]),
     ("fast_debug_copy", I, [V, V, I64, I, I64, I, V]),
     ("fast_comm_create_group", I, [I, I64, I64, ctypes.POINTER(V)]),
     ("fast_exec_group", I, [ctypes.POINTER(V), I, P_PLAN, ctypes.POINTER(V), I64, I, I64, V, V]),

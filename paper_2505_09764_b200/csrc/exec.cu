@@ -29,6 +29,7 @@
 
 #include "fastb200.h"
 #include "plan.cuh"
+#include "synth_dev.cuh"
 
 namespace {
 
@@ -73,15 +74,19 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
-// Spin until *p >= target (acquire, system scope).  false on timeout.
+// Spin until *p >= target (acquire).  false on timeout.  Polling backs off
+// exponentially (to 512 ns) so that many waiting CTAs do not flood one L2
+// line while the CTA they wait for is working.
 __device__ bool wait_geq(const uint64_t* p, uint64_t target, bool sys) {
   const uint64_t t0 = globaltimer();
+  unsigned sleep_ns = 32;
   int spins = 0;
   for (;;) {
     const uint64_t v = sys ? ld_acquire_sys(p) : ld_acquire_gpu(p);
     if (v >= target) return true;
-    if (++spins > 64) {
-      __nanosleep(128);
+    if (++spins > 8) {
+      __nanosleep(sleep_ns);
+      sleep_ns = sleep_ns < 512 ? sleep_ns * 2 : 512;
       if ((int64_t)(globaltimer() - t0) > kSpinLimitNs) return false;
     }
   }
@@ -105,6 +110,7 @@ struct ExecArgs {
   int64_t epoch;
   int64_t* timeline;
   int rank, world;
+  int skip_barrier;  // caller already synchronised the ranks for this epoch
 };
 
 __device__ __forceinline__ uint64_t* ctr(uint8_t* base, int idx) {
@@ -191,26 +197,35 @@ __device__ void cta_copy(uint8_t* dst, const uint8_t* src, int64_t len, bool nc)
 
 // ---- kernels ----------------------------------------------------------------
 
-__global__ void gather_demand_kernel(uint8_t* const* peers, const int64_t* row,
-                                     int64_t epoch, int rank, int world,
-                                     int64_t demand_off) {
-  // lane r (< world) writes this rank's row into rank r's demand buffer
-  // row[rank] (self bytes) goes to the self-size vector, D keeps a zero
-  // diagonal (DemandMatrix invariant, model.py:97-98)
+// P2P all-gather of this rank's demand row (one warp): row[rank] (own
+// segment, kept local) goes to the self-size vector, D keeps a zero
+// diagonal (DemandMatrix invariant, model.py:97-98).  Returns false on timeout.
+__device__ bool gather_rows(uint8_t* const* peers, const int64_t* row, int64_t epoch, int rank,
+                            int world, int64_t demand_off) {
   const int G = world;
   const int par = (int)(epoch & 1);
-  for (int r = threadIdx.x; r < world; r += blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (int r = lane; r < world; r += 32) {
     int64_t* dm = reinterpret_cast<int64_t*>(peers[r] + demand_off) + (int64_t)par * (G * G + G);
     for (int h = 0; h < G; ++h) dm[(int64_t)rank * G + h] = h == rank ? 0 : row[h];
     dm[(int64_t)G * G + rank] = row[rank];
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  __syncwarp();
+  bool ok = true;
+  if (lane == 0) {
     __threadfence_system();
     for (int r = 0; r < world; ++r) red_release_sys_add(ctr(peers[r], CTR_GATHER), 1);
-    if (!wait_geq(ctr(peers[rank], CTR_GATHER), (uint64_t)epoch * world, true))
-      atomicExch(reinterpret_cast<unsigned long long*>(ctr(peers[rank], CTR_STATUS)), 3ull);
+    ok = wait_geq(ctr(peers[rank], CTR_GATHER), (uint64_t)epoch * world, true);
   }
+  return __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
+}
+
+__global__ void gather_demand_kernel(uint8_t* const* peers, const int64_t* row,
+                                     int64_t epoch, int rank, int world,
+                                     int64_t demand_off) {
+  if (threadIdx.x >= 32) return;
+  if (!gather_rows(peers, row, epoch, rank, world, demand_off) && threadIdx.x == 0)
+    atomicExch(reinterpret_cast<unsigned long long*>(ctr(peers[rank], CTR_STATUS)), 3ull);
 }
 
 __device__ __forceinline__ int64_t nchunks(int64_t len, int64_t chunk) {
@@ -231,12 +246,178 @@ __global__ void __launch_bounds__(kExecThreads) raw_copy_kernel(uint8_t* dst, co
   }
 }
 
+// Device plan kernel: takes n_stages / synthesis status from device memory.
+// The plan is a sequential walk (one thread), so every input it touches and
+// its workspace are first staged into shared memory by the whole CTA when
+// they fit (`smem_ok`); otherwise it runs on the global copies.
+constexpr int kPlanThreads = 256;
+constexpr size_t kPlanSmemMax = 160 * 1024;
+
+__host__ __device__ inline size_t plan_smem_bytes(int n, int m) {
+  const int64_t G = (int64_t)n * m, K = (int64_t)n * n - 2 * n + 2;
+  size_t b = (size_t)fastplan::plan_ws_bytes(n, m) + 16;
+  b += (size_t)fastplan::plan_op_capacity(n, m, (int)K) * sizeof(fast_op);  // op buckets
+  b += (size_t)(G * G + G) * 8;        // D + self sizes
+  b += (size_t)K * 4 + 16;             // order
+  b += (size_t)K * n + 16;             // perm
+  b += (size_t)K * n * 8 + 16;         // stage bytes
+  return (b + 127) & ~(size_t)127;
+}
+
+// Stage the plan inputs + workspace in `psm` (whole CTA), then thread 0
+// walks the plan.  Caller guarantees the synthesis status is OK.
+__device__ void plan_cta(fastplan::PlanIn in, fastplan::PlanOut out, char* psm, int smem_ok) {
+  if (smem_ok) {
+    const int n = in.n, G = in.n * in.m, K = in.K;
+    char* p = psm;
+    char* ws = p; p += ((size_t)fastplan::plan_ws_bytes(in.n, in.m) + 16 + 15) & ~(size_t)15;
+    fast_op* scratch = (fast_op*)p; p += (size_t)in.op_cap * sizeof(fast_op);
+    int64_t* D = (int64_t*)p; p += (size_t)G * G * 8;
+    int64_t* ss = (int64_t*)p; p += (size_t)G * 8;
+    int32_t* ord = (int32_t*)p; p += ((size_t)K * 4 + 16 + 15) & ~(size_t)15;
+    int64_t* sb = (int64_t*)p; p += (size_t)K * n * 8 + 16;
+    uint8_t* pm = (uint8_t*)p;
+    for (int i = threadIdx.x; i < G * G; i += blockDim.x) D[i] = in.D[i];
+    for (int i = threadIdx.x; i < G; i += blockDim.x) ss[i] = in.send_self ? in.send_self[i] : 0;
+    for (int i = threadIdx.x; i < in.n_stages; i += blockDim.x) ord[i] = in.order[i];
+    // only the kept stages' rows are read by the plan
+    for (int i = threadIdx.x; i < in.n_stages * n; i += blockDim.x) {
+      const int k = in.order[i / n], u = i % n;
+      sb[(int64_t)k * n + u] = in.sbytes[(int64_t)k * n + u];
+      pm[(int64_t)k * n + u] = in.perm[(int64_t)k * n + u];
+    }
+    __syncthreads();
+    in.D = D;
+    in.send_self = in.send_self ? ss : nullptr;
+    in.order = ord;
+    in.sbytes = sb;
+    in.perm = pm;
+    out.ws = ws;
+    out.scratch = scratch;
+  }
+  if (threadIdx.x == 0) fastplan::plan_compile(in, out);
+}
+
+__global__ void __launch_bounds__(kPlanThreads)
+    fast_plan_kernel_dev(fastplan::PlanIn in, fastplan::PlanOut out, const int32_t* n_stages,
+                         const int32_t* sched_status, int smem_ok) {
+  extern __shared__ __align__(16) char psm[];
+  if (*sched_status != FAST_OK) {
+    if (threadIdx.x == 0) {
+      *out.n_ops = 0;
+      *out.status = *sched_status;
+    }
+    return;
+  }
+  in.n_stages = *n_stages;
+  plan_cta(in, out, psm, smem_ok);
+}
+
+// ---- fused single-launch path (n <= 6): everything before the exec loop ----
+constexpr int kFusedMaxN = 6;  // stage capacity <= 32: the decompose warp sorts
+
+struct FusedArgs {
+  const int64_t* counts;     // this rank's demand row (device)
+  int n, m;
+  int64_t demand_off;
+  fast_sched_bufs sched;     // B = 1
+  fastplan::PlanIn pin;      // shape / capacities (pointers filled in)
+  fastplan::PlanOut pout;
+};
+
+__host__ __device__ inline size_t fused_smem_bytes(int n, int m) {
+  const size_t tiles = (size_t)n * n * (m * m + 1) * 8;
+  return ((tiles + 127) & ~(size_t)127) + ((dec_smem_bytes_t<1>(n) + 127) & ~(size_t)127) +
+         plan_smem_bytes(n, m);
+}
+
+// CTA 0 of the fused exec kernel: gather -> balance -> decompose/strip/sort
+// -> plan, all on this device, before the entry barrier opens the exec loop.
+__device__ bool fused_prologue(const FusedArgs& f, uint8_t* const* peers, int rank, int world,
+                               int64_t epoch, char* sm, int64_t* tl) {
+  __shared__ int s_ok;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_ok = 1;
+  if (tl && tid == 0) tl[5] = (int64_t)globaltimer();
+  __syncthreads();
+  if (tid < 32 && !gather_rows(peers, f.counts, epoch, rank, world, f.demand_off) && tid == 0)
+    s_ok = 0;
+  const int n = f.n, m = f.m, G = n * m;
+  const int64_t* D = reinterpret_cast<const int64_t*>(peers[rank] + f.demand_off) +
+                     (epoch & 1) * ((int64_t)G * G + G);
+  if (tid == 0) *f.sched.status = FAST_OK;
+  if (tl && tid == 0) tl[6] = (int64_t)globaltimer();
+  __syncthreads();
+  if (!s_ok) return false;
+  // build_balance_plan + reduce_to_server_level, one thread per tile
+  const int TS = m * m + 1;
+  const int slots = m > 1 ? m - 1 : 1;
+  for (int t = tid; t < n * n; t += blockDim.x) {
+    const int i = t / n, j = t % n;
+    int64_t* tl = reinterpret_cast<int64_t*>(sm) + (int64_t)t * TS;
+    bool bad = false;
+    int64_t sum = 0;
+    for (int p = 0; p < m; ++p)
+      for (int q = 0; q < m; ++q) {
+        const int64_t v = D[(int64_t)(i * m + p) * G + j * m + q];
+        tl[p * m + q] = v;
+        if (v < 0) { bad = true; continue; }
+        if (i == j && p == q && v != 0) bad = true;
+        sum = sat_add(sum, v);
+      }
+    f.sched.server[i * n + j] = sum;
+    if (bad) {
+      raise_status(f.sched.status, FAST_EVALIDATION);
+    } else if (i != j) {
+      const int tidx = i * (n - 1) + (j < i ? j : j - 1);
+      int nm = balance_tile<0>(tl, m, f.sched.moves + (int64_t)tidx * slots, slots);
+      if (nm < 0) { raise_status(f.sched.status, FAST_EINVARIANT); nm = 0; }
+      f.sched.move_count[tidx] = nm;
+    }
+    for (int p = 0; p < m; ++p)
+      for (int q = 0; q < m; ++q)
+        f.sched.balanced[(int64_t)(i * m + p) * G + j * m + q] = tl[p * m + q];
+  }
+  __threadfence_block();
+  __syncthreads();
+  if (tl && tid == 0) tl[7] = (int64_t)globaltimer();
+  char* dsm = sm + (((size_t)n * n * TS * 8 + 127) & ~(size_t)127);
+  if (tid < 32)
+    decompose_one<1>(dsm, f.sched.server, 0, n, FAST_DEC_SERVER, 1, f.sched, tid);
+  __threadfence_block();
+  __syncthreads();
+  if (tl && tid == 0) tl[8 + 250] = (int64_t)globaltimer();
+  const int st = *f.sched.status;
+  fastplan::PlanOut out = f.pout;
+  if (st != FAST_OK) {
+    if (tid == 0) {
+      *out.n_ops = 0;
+      *out.status = st;
+    }
+    return true;  // the exec loop sees plan status != OK and moves nothing
+  }
+  fastplan::PlanIn in = f.pin;
+  in.D = D;
+  in.send_self = D + (int64_t)G * G;
+  in.n_stages = *f.sched.n_stages;
+  in.order = f.sched.stage_order;
+  in.perm = f.sched.stage_perm;
+  in.sbytes = f.sched.stage_bytes;
+  char* psm = dsm + ((dec_smem_bytes_t<1>(n) + 127) & ~(size_t)127);
+  plan_cta(in, out, psm, 1);
+  __threadfence();
+  __syncthreads();
+  return true;
+}
+
 // grid (blocks, ranks_in_launch): blockIdx.y selects the rank this CTA acts
 // for -- 1 in the multi-process mode, all `world` ranks in the one-GPU group
 // mode (cooperative launch, so every rank's CTAs are co-resident).
-__global__ void __launch_bounds__(kExecThreads) exec_kernel(ExecArgs a) {
+template <bool FUSED>
+__global__ void __launch_bounds__(kExecThreads) exec_kernel(ExecArgs a, FusedArgs f) {
   __shared__ unsigned long long s_red[3];  // recv chunks expected, producer / redist bytes
   __shared__ int s_fail;
+  extern __shared__ __align__(16) char fsm[];
   a.rank += blockIdx.y;
   a.send = a.sends[blockIdx.y];
   if (a.timeline) a.timeline += (int64_t)blockIdx.y * kTimelineStride;
@@ -245,17 +426,28 @@ __global__ void __launch_bounds__(kExecThreads) exec_kernel(ExecArgs a) {
   const int tid = threadIdx.x;
   const uint64_t epoch = (uint64_t)a.epoch;
   if (tid == 0) s_fail = 0;
+  // fused path: CTA 0 gathers D, synthesises the schedule and compiles the
+  // plan before the barrier; the other CTAs wait for GO as usual
+  if (FUSED && blockIdx.x == 0) {
+    if (!fused_prologue(f, a.peers, a.rank, a.world, a.epoch, fsm, a.timeline) && tid == 0)
+      s_fail = 1;
+    __syncthreads();
+  }
 
   // ---- entry barrier (CTA 0): reset the recv counter, arrive everywhere ---
   if (blockIdx.x == 0 && tid == 0) {
     if (a.timeline) a.timeline[0] = (int64_t)globaltimer();
-    reinterpret_cast<volatile uint64_t*>(me)[CTR_RECV] = 0;
+    // RECV is zero here: every exec leaves it zeroed at exit, and a peer can
+    // only signal epoch e after this rank published its demand row for e
     reinterpret_cast<volatile uint64_t*>(me)[CTR_WORK_P] = 0;
     reinterpret_cast<volatile uint64_t*>(me)[CTR_WORK_F] = 0;
     __threadfence_system();
     for (int r = 0; r < a.world; ++r)
       if (r != a.rank) red_release_sys_add(ctr(a.peers[r], CTR_ARRIVE), 1);
-    if (!wait_geq(ctr(me, CTR_ARRIVE), epoch * (a.world - 1), true)) s_fail = 1;
+    // fast_alltoallv: the demand all-gather of this epoch already proved that
+    // every peer entered it (hence finished the previous one); no wait needed
+    if (!a.skip_barrier && !wait_geq(ctr(me, CTR_ARRIVE), epoch * (a.world - 1), true))
+      s_fail = 1;
     st_release_gpu(ctr(me, CTR_GO), epoch);
     if (a.timeline) a.timeline[1] = (int64_t)globaltimer();
   } else if (tid == 0) {
@@ -345,72 +537,11 @@ __global__ void __launch_bounds__(kExecThreads) exec_kernel(ExecArgs a) {
   if (blockIdx.x == 0 && tid == 0) {
     if (a.timeline) a.timeline[3] = (int64_t)globaltimer();
     if (!s_fail && !wait_geq(ctr(me, CTR_RECV), (uint64_t)s_red[0], true)) s_fail = 1;
+    reinterpret_cast<volatile uint64_t*>(me)[CTR_RECV] = 0;  // ready for the next epoch
     if (a.timeline) a.timeline[4] = (int64_t)globaltimer();
   }
   __syncthreads();
   if (tid == 0 && s_fail) atomicExch(reinterpret_cast<unsigned long long*>(status), 3ull);
-}
-
-// Device plan kernel: takes n_stages / synthesis status from device memory.
-// The plan is a sequential walk (one thread), so every input it touches and
-// its workspace are first staged into shared memory by the whole CTA when
-// they fit (`smem_ok`); otherwise it runs on the global copies.
-constexpr int kPlanThreads = 256;
-constexpr size_t kPlanSmemMax = 160 * 1024;
-
-__host__ __device__ inline size_t plan_smem_bytes(int n, int m) {
-  const int64_t G = (int64_t)n * m, K = (int64_t)n * n - 2 * n + 2;
-  size_t b = (size_t)fastplan::plan_ws_bytes(n, m) + 16;
-  b += (size_t)fastplan::plan_op_capacity(n, m, (int)K) * sizeof(fast_op);  // op buckets
-  b += (size_t)(G * G + G) * 8;        // D + self sizes
-  b += (size_t)K * 4 + 16;             // order
-  b += (size_t)K * n + 16;             // perm
-  b += (size_t)K * n * 8 + 16;         // stage bytes
-  return (b + 127) & ~(size_t)127;
-}
-
-__global__ void __launch_bounds__(kPlanThreads)
-    fast_plan_kernel_dev(fastplan::PlanIn in, fastplan::PlanOut out, const int32_t* n_stages,
-                         const int32_t* sched_status, int smem_ok) {
-  extern __shared__ __align__(16) char psm[];
-  if (*sched_status != FAST_OK) {
-    if (threadIdx.x == 0) {
-      *out.n_ops = 0;
-      *out.status = *sched_status;
-    }
-    return;
-  }
-  in.n_stages = *n_stages;
-  if (smem_ok) {
-    const int n = in.n, G = in.n * in.m, K = in.K;
-    char* p = psm;
-    char* ws = p; p += ((size_t)fastplan::plan_ws_bytes(in.n, in.m) + 16 + 15) & ~(size_t)15;
-    fast_op* scratch = (fast_op*)p; p += (size_t)in.op_cap * sizeof(fast_op);
-    int64_t* D = (int64_t*)p; p += (size_t)G * G * 8;
-    int64_t* ss = (int64_t*)p; p += (size_t)G * 8;
-    int32_t* ord = (int32_t*)p; p += ((size_t)K * 4 + 16 + 15) & ~(size_t)15;
-    int64_t* sb = (int64_t*)p; p += (size_t)K * n * 8 + 16;
-    uint8_t* pm = (uint8_t*)p;
-    for (int i = threadIdx.x; i < G * G; i += blockDim.x) D[i] = in.D[i];
-    for (int i = threadIdx.x; i < G; i += blockDim.x) ss[i] = in.send_self ? in.send_self[i] : 0;
-    for (int i = threadIdx.x; i < in.n_stages; i += blockDim.x) ord[i] = in.order[i];
-    // only the kept stages' rows are read by the plan; copy them compactly
-    // (row k of the raw arrays -> row k, K rows at most)
-    for (int i = threadIdx.x; i < in.n_stages * n; i += blockDim.x) {
-      const int k = in.order[i / n], u = i % n;
-      sb[(int64_t)k * n + u] = in.sbytes[(int64_t)k * n + u];
-      pm[(int64_t)k * n + u] = in.perm[(int64_t)k * n + u];
-    }
-    __syncthreads();
-    in.D = D;
-    in.send_self = in.send_self ? ss : nullptr;
-    in.order = ord;
-    in.sbytes = sb;
-    in.perm = pm;
-    out.ws = ws;
-    out.scratch = scratch;
-  }
-  if (threadIdx.x == 0) fastplan::plan_compile(in, out);
 }
 
 }  // namespace
@@ -425,6 +556,7 @@ struct fast_comm {
   cudaIpcMemHandle_t handle;
   int opened;
   int64_t epoch;  // calls issued through fast_alltoallv
+  int no_fuse;    // 1: always use the multi-launch path
 };
 
 extern "C" {
@@ -465,10 +597,13 @@ int fast_plan_compile(const int64_t* D, const int64_t* send_self, int n, int m,
   out.scratch = nullptr;
   const size_t smem = plan_smem_bytes(n, m);
   const int smem_ok = smem <= kPlanSmemMax;
-  if (smem_ok && cudaFuncSetAttribute(fast_plan_kernel_dev,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem) != cudaSuccess)
-    return FAST_ECUDA;
+  static size_t plan_attr = 0;  // largest dynamic smem already granted
+  if (smem_ok && smem > plan_attr) {
+    if (cudaFuncSetAttribute(fast_plan_kernel_dev, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return FAST_ECUDA;
+    plan_attr = smem;
+  }
   fast_plan_kernel_dev<<<1, kPlanThreads, smem_ok ? smem : 0, (cudaStream_t)stream>>>(
       in, out, sched->n_stages, sched->status, smem_ok);
   return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
@@ -533,6 +668,7 @@ int fast_comm_create(int rank, int world, int max_gpus_per_row, int64_t recv_byt
   }
   c->peers_host = (uint8_t**)calloc(world, sizeof(uint8_t*));
   c->peers_host[rank] = c->base;
+  c->no_fuse = 1;  // the fused single launch is opt-in (fast_comm_set_fused)
   if (cudaMalloc(&c->peers_dev, sizeof(uint8_t*) * world) != cudaSuccess) {
     cudaFree(c->base);
     free(c->peers_host);
@@ -602,17 +738,30 @@ int fast_gather_demand(fast_comm* c, const int64_t* row, int64_t epoch, void* st
 // Every CTA of every rank must be resident at once (CTAs wait on flags that
 // other ranks' CTAs raise), so the grid may not exceed one wave.
 static int max_resident_blocks() {
+  static int cached = -1;  // one device per process (one rank per GPU)
+  if (cached >= 0) return cached;
   int dev = 0, sms = 0, per_sm = 0;
   if (cudaGetDevice(&dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, exec_kernel, kExecThreads, 0) !=
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, exec_kernel<false>, kExecThreads, 0) !=
           cudaSuccess)
     return 0;
-  return sms * per_sm;
+  cached = sms * per_sm;
+  return cached;
 }
+
+static int exec_launch(fast_comm* c, const fast_plan* plan, const void* send, int64_t epoch,
+                       int blocks, int64_t chunk_bytes, int64_t* timeline_ns, void* stream,
+                       int skip_barrier);
 
 int fast_exec(fast_comm* c, const fast_plan* plan, const void* send, int64_t epoch, int blocks,
               int64_t chunk_bytes, int64_t* timeline_ns, void* stream) {
+  return exec_launch(c, plan, send, epoch, blocks, chunk_bytes, timeline_ns, stream, 0);
+}
+
+static int exec_launch(fast_comm* c, const fast_plan* plan, const void* send, int64_t epoch,
+                       int blocks, int64_t chunk_bytes, int64_t* timeline_ns, void* stream,
+                       int skip_barrier) {
   if (!c || !c->opened || !plan || epoch < 1 || blocks < 1 || chunk_bytes < 16)
     return FAST_EVALIDATION;
   if (blocks > max_resident_blocks()) return FAST_EVALIDATION;
@@ -630,7 +779,10 @@ int fast_exec(fast_comm* c, const fast_plan* plan, const void* send, int64_t epo
   a.timeline = timeline_ns;
   a.rank = c->rank;
   a.world = c->world;
-  exec_kernel<<<blocks, kExecThreads, 0, (cudaStream_t)stream>>>(a);
+  a.skip_barrier = skip_barrier;
+  FusedArgs f;
+  memset(&f, 0, sizeof(f));
+  exec_kernel<false><<<blocks, kExecThreads, 0, (cudaStream_t)stream>>>(a, f);
   return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
 }
 
@@ -675,8 +827,10 @@ int fast_exec_group(fast_comm* const* comms, int world, const fast_plan* plan,
   a.timeline = timeline_ns;
   a.rank = 0;
   a.world = world;
-  void* args[] = {&a};
-  cudaError_t e = cudaLaunchCooperativeKernel((const void*)exec_kernel, dim3(blocks, world),
+  FusedArgs f;
+  memset(&f, 0, sizeof(f));
+  void* args[] = {&a, &f};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)exec_kernel<false>, dim3(blocks, world),
                                               dim3(kExecThreads), args, 0,
                                               (cudaStream_t)stream);
   return e == cudaSuccess ? FAST_OK : FAST_ECUDA;
@@ -695,11 +849,84 @@ int fast_debug_copy(void* dst, const void* src, int64_t bytes, int blocks, int64
   return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
 }
 
+// Single-launch fused path (n <= 6): gather, synthesis and plan run in CTA 0
+// of the exec kernel itself.
+static int launch_fused(fast_comm* c, const void* send, const int64_t* counts, int n, int m,
+                        const fast_sched_bufs* sched, const fast_plan* plan, int blocks,
+                        int64_t chunk_bytes, int64_t* timeline_ns, cudaStream_t stream) {
+  const size_t smem = fused_smem_bytes(n, m);
+  static size_t fused_attr = 0;
+  static int fused_resident = 0;
+  if (smem > fused_attr) {
+    if (cudaFuncSetAttribute(exec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return FAST_ECUDA;
+    int dev = 0, sms = 0, per_sm = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, exec_kernel<true>, kExecThreads,
+                                                      smem) != cudaSuccess)
+      return FAST_ECUDA;
+    fused_attr = smem;
+    fused_resident = sms * per_sm;
+  }
+  if (blocks > fused_resident) return FAST_EVALIDATION;
+  const int64_t e = c->epoch + 1;
+  c->epoch = e;
+  ExecArgs a;
+  memset(&a, 0, sizeof(a));
+  a.peers = c->peers_dev;
+  a.ops = plan->ops;
+  a.n_ops = plan->n_ops;
+  a.plan_status = plan->status;
+  a.sends[0] = (const uint8_t*)send;
+  a.recv_off = c->recv_off;
+  a.staging_off = c->staging_off;
+  a.chunk = chunk_bytes & ~(int64_t)15;
+  a.epoch = e;
+  a.timeline = timeline_ns;
+  a.rank = c->rank;
+  a.world = c->world;
+  a.skip_barrier = 1;  // the in-kernel demand all-gather synchronises the ranks
+  FusedArgs f;
+  memset(&f, 0, sizeof(f));
+  f.counts = counts;
+  f.n = n;
+  f.m = m;
+  f.demand_off = c->demand_off;
+  f.sched = *sched;
+  f.pin.n = n;
+  f.pin.m = m;
+  f.pin.K = n * n - 2 * n + 2;
+  f.pin.recv_cap = c->recv_bytes;
+  f.pin.staging_cap = c->staging_bytes;
+  f.pin.op_cap = plan->op_capacity;
+  f.pin.chunk = a.chunk;
+  f.pout.ops = plan->ops;
+  f.pout.n_ops = plan->n_ops;
+  f.pout.staging_used = plan->staging_used;
+  f.pout.status = plan->status;
+  f.pout.ws = plan->workspace;
+  f.pout.scratch = nullptr;
+  exec_kernel<true><<<blocks, kExecThreads, smem, stream>>>(a, f);
+  return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
+}
+
+int fast_comm_set_fused(fast_comm* c, int enable) {
+  if (!c) return FAST_EVALIDATION;
+  c->no_fuse = enable ? 0 : 1;
+  return FAST_OK;
+}
+
 int fast_alltoallv(fast_comm* c, const void* send, const int64_t* counts, int n, int m,
                    const fast_sched_bufs* sched, const fast_plan* plan, int blocks,
                    int64_t chunk_bytes, int64_t* timeline_ns, void* stream) {
   if (!c || !c->opened || !send || !counts || !sched || !plan) return FAST_EVALIDATION;
-  if ((int64_t)n * m != c->world) return FAST_EVALIDATION;
+  if ((int64_t)n * m != c->world || n < 2 || m > FAST_MAX_GPUS_PER_SERVER || chunk_bytes < 16)
+    return FAST_EVALIDATION;
+  if (!c->no_fuse && n <= kFusedMaxN && fused_smem_bytes(n, m) <= 200 * 1024)
+    return launch_fused(c, send, counts, n, m, sched, plan, blocks, chunk_bytes, timeline_ns,
+                        (cudaStream_t)stream);
   const int64_t e = c->epoch + 1;
   int rc = fast_gather_demand(c, counts, e, stream);
   if (rc != FAST_OK) return rc;
@@ -710,7 +937,7 @@ int fast_alltoallv(fast_comm* c, const void* send, const int64_t* counts, int n,
   rc = fast_plan_compile(D, D + (int64_t)c->world * c->world, n, m, sched, c->recv_bytes,
                          c->staging_bytes, chunk_bytes, plan, stream);
   if (rc != FAST_OK) return rc;
-  return fast_exec(c, plan, send, e, blocks, chunk_bytes, timeline_ns, stream);
+  return exec_launch(c, plan, send, e, blocks, chunk_bytes, timeline_ns, stream, 1);
 }
 
 int64_t fast_comm_epoch(const fast_comm* c) { return c ? c->epoch : -1; }

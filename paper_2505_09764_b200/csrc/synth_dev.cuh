@@ -1,0 +1,644 @@
+// synth_dev.cuh -- device building blocks of FAST synthesis, shared by the
+// batched kernels (synth.cu) and the fused single-matrix executor path
+// (exec.cu): balance_senders on one tile, the warp-level Birkhoff
+// decomposition with inline strip and (n <= 6) sort.  See synth.cu for the
+// design notes; every function cites the reference lines it replaces.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fastb200.h"
+
+#ifndef DPROF_T
+#define DPROF_T(var)
+#define DPROF_ADD(slot, val)
+#endif
+
+namespace {
+
+constexpr int64_t kMaxSafeTotal = int64_t(1) << 62;  // model.py:26
+
+__device__ __forceinline__ int64_t sat_add(int64_t s, int64_t v) {
+  // s, v >= 0; saturate at 2^62 so that a later ">= 2^62" test is exact.
+  return (v >= kMaxSafeTotal - s) ? kMaxSafeTotal : s + v;
+}
+
+__device__ __forceinline__ void raise_status(int32_t* st, int code) {
+  atomicMax(st, code);
+}
+
+__host__ __device__ __forceinline__ int stage_cap(int n) {
+  return n * n - 2 * n + 2;
+}
+
+// ---------------------------------------------------------------------------
+// balance_senders (balance.py:77-126) on one m x m tile in shared memory.
+// Returns the number of moves, or -1 if an invariant breaks.
+template <int M>
+__device__ int balance_tile(int64_t* __restrict__ t, const int m_rt,
+                            fast_move* __restrict__ out, const int slots) {
+  constexpr int MM = M ? M : FAST_MAX_GPUS_PER_SERVER;
+  const int m = M ? M : m_rt;
+  int64_t dev[MM];
+  int64_t total = 0;
+#pragma unroll
+  for (int p = 0; p < MM; ++p) {
+    int64_t s = 0;
+    if (p < m)
+      for (int q = 0; q < m; ++q) s += t[p * m + q];
+    dev[p] = s;
+    total += s;
+  }
+  const int64_t base = total / m, extra = total % m;
+#pragma unroll
+  for (int p = 0; p < MM; ++p)
+    if (p < m) dev[p] -= base + (p < extra ? 1 : 0);
+
+  int nmoves = 0;
+  for (;;) {
+    // over[0]: largest positive deviation, lowest index on ties;
+    // under[0]: most negative deviation, lowest index on ties.
+    int g = -1, h = -1;
+    int64_t dg = 0, dh = 0;
+#pragma unroll
+    for (int p = 0; p < MM; ++p) {
+      if (p < m) {
+        const int64_t d = dev[p];
+        if (d > dg) { dg = d; g = p; }
+        if (d < dh) { dh = d; h = p; }
+      }
+    }
+    if (g < 0) return nmoves;
+    if (h < 0 || nmoves >= slots) return -1;
+    const int64_t chunk = dg < -dh ? dg : -dh;
+    int64_t left = chunk;
+    int guard = 0;
+    int64_t* rg = t + g * m;
+    int64_t* rh = t + h * m;
+    while (left > 0) {
+      int q = 0;  // np.argmax: first maximum of row g
+      int64_t best = rg[0];
+      for (int c = 1; c < m; ++c) {
+        const int64_t x = rg[c];
+        if (x > best) { best = x; q = c; }
+      }
+      const int64_t take = left < best ? left : best;
+      if (take <= 0 || ++guard > m) return -1;
+      rg[q] -= take;
+      rh[q] += take;
+      left -= take;
+    }
+#pragma unroll
+    for (int p = 0; p < MM; ++p) {
+      if (p == g) dev[p] -= chunk;
+      if (p == h) dev[p] += chunk;
+    }
+    fast_move mv;
+    mv.bytes = chunk;
+    mv.from_gpu = g;
+    mv.to_gpu = h;
+    out[nmoves++] = mv;
+  }
+}
+
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int64_t warp_min_i64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t x = __shfl_xor_sync(0xffffffffu, v, o);
+    v = x < v ? x : v;
+  }
+  return v;
+}
+__device__ __forceinline__ int64_t warp_max_i64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t x = __shfl_xor_sync(0xffffffffu, v, o);
+    v = x > v ? x : v;
+  }
+  return v;
+}
+__device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Per-matrix workspace: work matrix n*n int64, then sort keys (K x u64,
+// K x u32) for the kept stages.
+__host__ __device__ __forceinline__ size_t dec_ws_bytes_per_matrix(int n) {
+  const size_t K = (size_t)stage_cap(n);
+  size_t b = (size_t)n * n * 8 + K * 8 + K * 4;
+  return (b + 255) & ~(size_t)255;
+}
+
+// ---------------------------------------------------------------------------
+// Decomposition: one warp per matrix (birkhoff.py:75-252).
+//
+// State split:
+//   shared  sup[u]   support bitset of row u (work[u][v] > 0), NWP words
+//           supc[v]  copy of sup[cm[v]]: support of the row matched to v, so
+//                    one DFS step is a single 16-B shared load
+//           cm[v]    col_match; newcol[u] row's column after re-augmentation
+//           pick[k]  DFS stack: column chosen at depth k
+//   regs    lane owns rows u = r*32 + lane (r < NW): matched column, work
+//           value of its matched cell, and the off-diagonal demand there
+//   global  work[u][v] (embedded matrix, written back when a row leaves a
+//           non-zero cell) -- only touched when a row's match changes.
+// strip_auxiliary (birkhoff.py:225-252) is applied inline with the closed
+// form charged = min(w, max(0, work_before - off)): a cell's auxiliary bytes
+// are paid first, so aux_left = max(0, aux - peeled) = max(0, work - off).
+
+template <int NW>
+struct DecSh {
+  static constexpr int NQ = (NW + 1) / 2;   // u64 words per support row
+  static constexpr int NWP = 2 * NQ;        // u32 words per support row
+  uint32_t* sup;   // [n][NWP]
+  uint32_t* supc;  // [n][NWP]
+  int64_t* R;      // [n+1]
+  int64_t* C;      // [n+1]
+  int64_t* auxl;   // [2n+2] aux_left of the NW-corner staircase cells
+  int16_t* alo;    // [n] first column of row u's staircase range
+  int16_t* ahi;    // [n] last column (alo - 1 when empty)
+  int16_t* aoff;   // [n] offset of row u's range in auxl
+  int16_t* cm;     // [n]
+  int16_t* newcol; // [n]
+  int16_t* pick;   // [n]
+  int16_t* freed;  // [n]
+  uint32_t* chg;   // [NWP] rows whose match changed (bit r%32 of word r/32)
+  uint32_t* freeb; // [NWP] free columns (cm < 0), support-bitset layout
+};
+
+template <int NW>
+__host__ __device__ __forceinline__ size_t dec_smem_bytes_t(int n) {
+  constexpr int NWP = 2 * ((NW + 1) / 2);
+  size_t b = 2 * (size_t)n * NWP * 4;      // sup, supc
+  b += 2 * (size_t)(n + 1) * 8;            // R, C
+  b += (size_t)(2 * n + 2) * 8;            // auxl
+  b += 3 * (size_t)n * 2 + 16;             // alo ahi aoff
+  b += 4 * (size_t)n * 2;                  // cm newcol pick freed
+  b += NWP * 4 + 16;                       // chg
+  b += NWP * 4 + 16;                       // freeb
+  return (b + 15) & ~(size_t)15;
+}
+
+template <int NW>
+__device__ __forceinline__ DecSh<NW> dec_carve_t(char* p, int n) {
+  constexpr int NWP = DecSh<NW>::NWP;
+  DecSh<NW> s;
+  s.sup = (uint32_t*)p; p += (size_t)n * NWP * 4;
+  s.supc = (uint32_t*)p; p += (size_t)n * NWP * 4;
+  s.R = (int64_t*)p; p += (size_t)(n + 1) * 8;
+  s.C = (int64_t*)p; p += (size_t)(n + 1) * 8;
+  s.auxl = (int64_t*)p; p += (size_t)(2 * n + 2) * 8;
+  s.chg = (uint32_t*)p; p += NWP * 4 + 16;
+  s.freeb = (uint32_t*)p; p += NWP * 4 + 16;
+  s.cm = (int16_t*)p; p += n * 2;
+  s.newcol = (int16_t*)p; p += n * 2;
+  s.pick = (int16_t*)p; p += n * 2;
+  s.freed = (int16_t*)p; p += n * 2;
+  s.alo = (int16_t*)p; p += n * 2;
+  s.ahi = (int16_t*)p; p += n * 2;
+  s.aoff = (int16_t*)p;
+  return s;
+}
+
+// Column layout of the support bitsets: u64 word q holds columns 64q..64q+63
+// with column 64q + b at bit 63 - b, so "first column of row & ~seen" is a
+// count-leading-zeros per 64-bit half.  In the u32 view that is word
+// (v >> 5) ^ 1, bit 31 - (v & 31).
+__device__ __forceinline__ int colword(int v) { return (v >> 5) ^ 1; }
+__device__ __forceinline__ uint32_t colbit(int v) { return 0x80000000u >> (v & 31); }
+
+template <int NW>
+__device__ __forceinline__ void load_row64(const uint32_t* src, uint64_t& r0, uint64_t& r1) {
+  if constexpr (DecSh<NW>::NQ == 2) {
+    const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(src);
+    r0 = x.x;
+    r1 = x.y;
+  } else {
+    r0 = *reinterpret_cast<const uint64_t*>(src);
+    r1 = 0ull;
+  }
+}
+
+// Kuhn augment(root) with a fresh `seen` (birkhoff.py:172-180), one thread.
+// When a frame resumes after a failed child every support column left of
+// the failed one is already seen, so "first column of support & ~seen" is
+// exactly the reference's next v and no resume cursor is needed.  Returns
+// the depth of the successful path (pick[k] = column taken at depth k,
+// pick[depth] free) or -1.
+__device__ __forceinline__ int clz64(uint64_t x) {  // 64 for x == 0
+  const uint32_t hi = (uint32_t)(x >> 32), lo = (uint32_t)x;
+  return hi ? __clz(hi) : 32 + __clz(lo);
+}
+
+template <int NW>
+__device__ int dfs_search(const DecSh<NW>& s, const int root, uint64_t free0,
+                          uint64_t free1) {
+  constexpr int NWP = DecSh<NW>::NWP;
+  uint64_t seen0 = 0ull, seen1 = 0ull, r0, r1;
+  load_row64<NW>(s.sup + root * NWP, r0, r1);
+  int sp = 0;
+  for (;;) {
+    const int z0 = clz64(r0 & ~seen0), z1 = clz64(r1 & ~seen1);
+    const int v = z0 < 64 ? z0 : 64 + z1;  // 128: no unseen support column
+    uint64_t n0, n1;
+    load_row64<NW>(s.supc + (v & 127) * NWP, n0, n1);  // speculative next row
+    if (__builtin_expect(v == 128, 0)) {
+      if (sp == 0) return -1;
+      --sp;
+      load_row64<NW>(sp == 0 ? s.sup + root * NWP : s.supc + s.pick[sp - 1] * NWP, r0, r1);
+      continue;
+    }
+    const uint64_t m = 0x8000000000000000ull >> (v & 63);
+    const bool hi = v >= 64;
+    const uint64_t fm = (hi ? free1 : free0) & m;
+    seen0 |= hi ? 0ull : m;
+    seen1 |= hi ? m : 0ull;
+    s.pick[sp] = (int16_t)v;
+    if (fm) return sp;
+    ++sp;
+    r0 = n0;
+    r1 = n1;
+  }
+}
+
+// Lane 0 searches, the result is broadcast (the other lanes wait).
+template <int NW>
+__device__ __forceinline__ int dfs_warp(const DecSh<NW>& s, const int root) {
+  int depth = 0;
+  if ((threadIdx.x & 31) == 0) {
+    const uint64_t* fq = reinterpret_cast<const uint64_t*>(s.freeb);
+    depth = dfs_search<NW>(s, root, fq[0], DecSh<NW>::NQ == 2 ? fq[1] : 0ull);
+  }
+  return __shfl_sync(0xffffffffu, depth, 0);
+}
+
+// Apply an augmenting path (warp-wide): cm[pick[k]] = row_k where row_0 =
+// root and row_{k+1} = old cm[pick[k]]; record new columns, refresh supc.
+template <int NW>
+__device__ __forceinline__ void apply_path(const DecSh<NW>& s, const int root,
+                                           const int depth, const int lane) {
+  constexpr int NWP = DecSh<NW>::NWP;
+  __syncwarp();  // lane 0's pick[] writes visible to the warp
+  int rows[(FAST_MAX_SERVERS + 31) / 32];
+#pragma unroll
+  for (int j = 0; j < (FAST_MAX_SERVERS + 31) / 32; ++j) {
+    const int k = j * 32 + lane;
+    rows[j] = (k <= depth) ? (k == 0 ? root : s.cm[s.pick[k - 1]]) : -1;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < (FAST_MAX_SERVERS + 31) / 32; ++j) {
+    const int k = j * 32 + lane;
+    if (k <= depth) {
+      const int v = s.pick[k], r = rows[j];
+      s.cm[v] = (int16_t)r;
+      s.newcol[r] = (int16_t)v;
+#pragma unroll
+      for (int w = 0; w < NWP; ++w) s.supc[v * NWP + w] = s.sup[r * NWP + w];
+      atomicOr(&s.chg[r >> 5], 1u << (r & 31));
+      if (k == depth) atomicAnd(&s.freeb[colword(v)], ~colbit(v));  // matched now
+    }
+  }
+  __syncwarp();
+}
+
+// aux_left of cell (u, v): a slot of the row's staircase range, or -1.
+template <int NW>
+__device__ __forceinline__ int aux_slot(const DecSh<NW>& s, int u, int v) {
+  return (v >= s.alo[u] && v <= s.ahi[u]) ? s.aoff[u] + v - s.alo[u] : -1;
+}
+
+// The whole decomposition of matrix b by one warp; `wsm` is this warp's
+// dec_smem_bytes_t<NW>(n) bytes of shared memory.
+template <int NW>
+__device__ void decompose_one(char* wsm, const int64_t* __restrict__ S_all, const int b,
+                              const int n, const int mode, const int check_total,
+                              const fast_sched_bufs& out, const int lane) {
+  constexpr int NWP = DecSh<NW>::NWP;
+  const int K = stage_cap(n);
+  DecSh<NW> s = dec_carve_t<NW>(wsm, n);
+  int64_t* work = (int64_t*)((char*)out.workspace + (size_t)b * dec_ws_bytes_per_matrix(n));
+  uint64_t* key_w = (uint64_t*)(work + (size_t)n * n);
+  uint32_t* key_t = (uint32_t*)(key_w + K);
+  const int64_t* S = S_all + (int64_t)b * n * n;
+  int32_t* status = out.status + b;
+  int64_t* aux_out = out.aux + (int64_t)b * n * n;
+
+  int st = check_total ? *status : FAST_OK;
+
+  // ---- row/column sums of the off-diagonal demand ------------------------
+  int64_t colsum[NW];
+  int64_t rowmax = 0, tot = 0, row0 = 0;
+  bool neg = false, ds_bad = false;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) colsum[w] = 0;
+  for (int u = 0; u < n; ++u) {
+    int64_t rs = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const int v = w * 32 + lane;
+      if (v < n) {
+        int64_t x = S[(int64_t)u * n + v];
+        if (x < 0) neg = true;
+        tot = sat_add(tot, x < 0 ? 0 : x);
+        if (mode == FAST_DEC_SERVER && u == v) x = 0;
+        colsum[w] += x;
+        rs += x;
+      }
+    }
+    rs = warp_sum_i64(rs);
+    if (u == 0) row0 = rs;
+    if (mode == FAST_DEC_DOUBLY_STOCHASTIC && rs != row0) ds_bad = true;
+    rowmax = rs > rowmax ? rs : rowmax;
+    if (lane == 0) s.R[u + 1] = rs;  // row sums; turned into a prefix below
+  }
+  int64_t colmax = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const int v = w * 32 + lane;
+    if (v < n) {
+      colmax = colsum[w] > colmax ? colsum[w] : colmax;
+      if (mode == FAST_DEC_DOUBLY_STOCHASTIC && colsum[w] != row0) ds_bad = true;
+    }
+  }
+  colmax = warp_max_i64(colmax);
+  neg = __any_sync(0xffffffffu, neg);
+  ds_bad = __any_sync(0xffffffffu, ds_bad);
+  int64_t all = 0;
+  for (int l = 0; l < 32; ++l) all = sat_add(all, __shfl_sync(0xffffffffu, tot, l));
+  if (st == FAST_OK) {
+    if (neg || ds_bad) st = FAST_EVALIDATION;
+    if (check_total && all >= kMaxSafeTotal) st = FAST_EVALIDATION;
+  }
+  const int64_t common =
+      mode == FAST_DEC_DOUBLY_STOCHASTIC ? row0 : (rowmax > colmax ? rowmax : colmax);
+  if (st != FAST_OK) {
+    if (lane == 0) {
+      *status = st;
+      out.common_sum[b] = 0;
+      out.n_raw[b] = 0;
+      out.n_stages[b] = 0;
+    }
+    return;
+  }
+
+  // ---- embedding: northwest corner == interval overlap of deficit prefixes
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const int v = w * 32 + lane;
+    if (v < n) s.C[v + 1] = common - colsum[w];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    s.R[0] = 0;
+    s.C[0] = 0;
+    for (int u = 0; u < n; ++u) s.R[u + 1] = s.R[u] + (common - s.R[u + 1]);
+    for (int v = 0; v < n; ++v) s.C[v + 1] += s.C[v];
+  }
+  for (int u = lane; u < n; u += 32) s.cm[u] = -1;
+  if (lane < NWP) {
+    s.chg[lane] = 0u;
+    s.freeb[lane] = 0u;
+  }
+  __syncwarp();
+  for (int v = lane; v < n; v += 32) atomicOr(&s.freeb[colword(v)], colbit(v));
+  __syncwarp();
+  for (int u = 0; u < n; ++u) {
+    const int64_t r0 = s.R[u], r1 = s.R[u + 1];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const int v = w * 32 + lane;
+      int64_t e = 0;
+      if (v < n) {
+        int64_t off = S[(int64_t)u * n + v];
+        int64_t a = 0;
+        if (mode == FAST_DEC_SERVER) {
+          if (u == v) off = 0;
+          const int64_t lo = r0 > s.C[v] ? r0 : s.C[v];
+          const int64_t hi = r1 < s.C[v + 1] ? r1 : s.C[v + 1];
+          a = hi > lo ? hi - lo : 0;
+        }
+        e = off + a;
+        aux_out[(int64_t)u * n + v] = a;
+        work[(int64_t)u * n + v] = e;
+      }
+      const uint32_t bits = __brev(__ballot_sync(0xffffffffu, e > 0));
+      if (lane == 0) s.sup[u * NWP + (w ^ 1)] = bits;
+    }
+    if (NWP > NW && lane == 0) s.sup[u * NWP + ((NWP - 1) ^ 1)] = 0u;
+  }
+  if (lane == 0) {
+    out.common_sum[b] = common;
+    // NW-corner staircase: row u's aux cells are the contiguous columns whose
+    // deficit interval overlaps [R_u, R_u+1); consecutive rows share at most
+    // one column, so all of them fit in 2n slots (aux_left lives here).
+    int v = 0, at = 0;
+    for (int u = 0; u < n; ++u) {
+      const int64_t r0 = s.R[u], r1 = s.R[u + 1];
+      if (mode != FAST_DEC_SERVER || r1 == r0) {
+        s.alo[u] = 0; s.ahi[u] = -1; s.aoff[u] = (int16_t)at;
+        continue;
+      }
+      while (v < n - 1 && s.C[v + 1] <= r0) ++v;
+      int e = v;
+      while (e < n - 1 && s.C[e + 1] < r1) ++e;
+      s.alo[u] = (int16_t)v; s.ahi[u] = (int16_t)e; s.aoff[u] = (int16_t)at;
+      for (int c = v; c <= e; ++c) {
+        const int64_t lo = r0 > s.C[c] ? r0 : s.C[c];
+        const int64_t hi = r1 < s.C[c + 1] ? r1 : s.C[c + 1];
+        s.auxl[at++] = hi > lo ? hi - lo : 0;
+      }
+    }
+  }
+  __syncwarp();
+  if (common == 0) {
+    if (lane == 0) {
+      out.n_raw[b] = 0;
+      out.n_stages[b] = 0;
+      *status = FAST_OK;
+    }
+    return;
+  }
+
+  // ---- initial Kuhn matching (birkhoff.py:182-186) -----------------------
+  for (int u = 0; u < n; ++u) {
+    const int depth = dfs_warp<NW>(s, u);
+    if (depth < 0) { st = FAST_EINVARIANT; break; }
+    apply_path<NW>(s, u, depth, lane);
+  }
+  if (st != FAST_OK) {
+    if (lane == 0) { *status = st; out.n_raw[b] = 0; out.n_stages[b] = 0; }
+    return;
+  }
+  // lane-owned row state
+  int rcol[NW];
+  int64_t mv[NW], am[NW];
+#pragma unroll
+  for (int r = 0; r < NW; ++r) {
+    const int u = r * 32 + lane;
+    rcol[r] = -1;
+    mv[r] = INT64_MAX;
+    am[r] = 0;
+    if (u < n) {
+      const int v = s.newcol[u];
+      rcol[r] = v;
+      mv[r] = work[(int64_t)u * n + v];
+      const int sl = aux_slot<NW>(s, u, v);
+      am[r] = sl >= 0 ? s.auxl[sl] : 0;
+    }
+  }
+  if (lane < NWP) s.chg[lane] = 0u;
+  __syncwarp();
+
+  // ---- peel loop (birkhoff.py:190-219) fused with strip -----------------
+  int64_t remaining = common;
+  int k = 0, kept = 0;
+  int64_t* wout = out.stage_weight + (int64_t)b * K;
+  uint8_t* pout = out.stage_perm + (int64_t)b * K * n;
+  int64_t* bout = out.stage_bytes + (int64_t)b * K * n;
+  while (remaining > 0) {
+    DPROF_T(t0);
+    if (k >= K) { st = FAST_EINVARIANT; break; }
+    int64_t wl = INT64_MAX;
+#pragma unroll
+    for (int r = 0; r < NW; ++r) wl = mv[r] < wl ? mv[r] : wl;
+    const int64_t weight = warp_min_i64(wl);
+    if (weight <= 0) { st = FAST_EINVARIANT; break; }
+    remaining -= weight;
+    int src0 = -1, nfreed = 0, dst0 = 0;
+#pragma unroll
+    for (int r = 0; r < NW; ++r) {
+      const int u = r * 32 + lane;
+      bool real_pos = false, fr = false;
+      const int vsave = rcol[r];
+      if (u < n) {
+        const int v = rcol[r];
+        // strip_auxiliary (birkhoff.py:225-252): the cell pays aux first
+        const int64_t charged = am[r] < weight ? am[r] : weight;
+        const int64_t real = weight - charged;
+        am[r] -= charged;
+        mv[r] -= weight;
+        __stcs(bout + (int64_t)k * n + u, real);
+        pout[(int64_t)k * n + u] = (uint8_t)v;
+        real_pos = real > 0;
+        if (mv[r] == 0) {
+          s.sup[u * NWP + colword(v)] &= ~colbit(v);
+          fr = remaining > 0;
+        }
+      }
+      const uint32_t rb = __ballot_sync(0xffffffffu, real_pos);
+      if (src0 < 0 && rb) {
+        src0 = r * 32 + __ffs(rb) - 1;
+        dst0 = __shfl_sync(0xffffffffu, vsave, __ffs(rb) - 1);
+      }
+      const uint32_t fb = __ballot_sync(0xffffffffu, fr);
+      if (fr) {
+        s.freed[nfreed + __popc(fb & ((1u << lane) - 1u))] = (int16_t)u;
+        s.cm[rcol[r]] = -1;  // unmatch (birkhoff.py:210-214)
+        atomicOr(&s.freeb[colword(rcol[r])], colbit(rcol[r]));
+        rcol[r] = -1;
+      }
+      nfreed += __popc(fb);
+    }
+    if (lane == 0) {
+      wout[k] = weight;
+      if (src0 >= 0) {
+        // dst of src0 = the column src0 was matched to in this stage
+        key_w[kept] = (uint64_t)weight;
+        key_t[kept] = ((uint32_t)src0 << 24) | ((uint32_t)dst0 << 16) | (uint32_t)k;
+      }
+    }
+    if (src0 >= 0) ++kept;
+    ++k;
+    if (remaining == 0) break;
+    __syncwarp();
+    DPROF_T(t1);
+    DPROF_ADD(0, t1 - t0);
+    // re-augment freed rows in index order (birkhoff.py:215-219)
+    for (int f = 0; f < nfreed; ++f) {
+      const int u = s.freed[f];
+      DPROF_T(ta);
+      const int depth = dfs_warp<NW>(s, u);
+      DPROF_T(tb);
+      if (depth < 0) { st = FAST_EINVARIANT; break; }
+      apply_path<NW>(s, u, depth, lane);
+      DPROF_T(tc);
+      DPROF_ADD(1, tb - ta);
+      DPROF_ADD(2, tc - tb);
+      DPROF_ADD(4, depth + 1);
+    }
+    if (st != FAST_OK) break;
+    DPROF_T(t2);
+    // rows whose cell changed: write the old (non-zero) value back, fetch
+    // the new cell; all loads are issued before any is consumed.
+    uint32_t chg[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) chg[w] = s.chg[w];
+    __syncwarp();
+    if (lane < NWP) s.chg[lane] = 0u;
+    int64_t nv[NW];
+    bool moved[NW];
+#pragma unroll
+    for (int r = 0; r < NW; ++r) {
+      const int u = r * 32 + lane;
+      const int nc = (u < n && ((chg[r] >> lane) & 1u)) ? s.newcol[u] : rcol[r];
+      moved[r] = nc != rcol[r];
+      if (moved[r]) {
+        if (rcol[r] >= 0) {
+          work[(int64_t)u * n + rcol[r]] = mv[r];
+          const int so = aux_slot<NW>(s, u, rcol[r]);
+          if (so >= 0) s.auxl[so] = am[r];
+        }
+        rcol[r] = nc;
+        nv[r] = work[(int64_t)u * n + nc];
+        const int sn = aux_slot<NW>(s, u, nc);
+        am[r] = sn >= 0 ? s.auxl[sn] : 0;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NW; ++r)
+      if (moved[r]) mv[r] = nv[r];
+    __syncwarp();
+    DPROF_T(t3);
+    DPROF_ADD(3, t3 - t2);
+    DPROF_ADD(5, 1);
+  }
+
+  // ---- final invariants (birkhoff.py:216-221, :273-277): every cell peeled
+  if (st == FAST_OK) {
+    bool left = remaining != 0;
+    for (int c = lane; c < n * NWP; c += 32) left |= s.sup[c] != 0u;
+    if (__any_sync(0xffffffffu, left)) st = FAST_EINVARIANT;
+  }
+  // small stage capacity (n <= 6): sort_stages_ascending here with a warp
+  // bitonic network on (weight, src0|dst0|raw index) and skip sort_kernel
+  if (K <= 32 && st == FAST_OK && kept > 0) {
+    __syncwarp();
+    uint64_t w = lane < kept ? key_w[lane] : ~0ull;
+    uint32_t t = lane < kept ? key_t[lane] : ~0u;
+#pragma unroll
+    for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        const uint64_t w2 = __shfl_xor_sync(0xffffffffu, w, j);
+        const uint32_t t2 = __shfl_xor_sync(0xffffffffu, t, j);
+        const bool asc = (lane & kk) == 0;
+        const bool lower = (lane & j) == 0;
+        const bool gt = w > w2 || (w == w2 && t > t2);
+        if ((lower == asc) ? gt : !gt) { w = w2; t = t2; }
+      }
+    }
+    if (lane < kept) out.stage_order[(int64_t)b * K + lane] = (int32_t)(t & 0xffffu);
+  }
+  if (lane == 0) {
+    *status = st;
+    out.n_raw[b] = k;
+    out.n_stages[b] = st == FAST_OK ? kept : 0;
+  }
+}
+
+
+}  // namespace

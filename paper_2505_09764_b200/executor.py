@@ -172,6 +172,11 @@ class FastComm:
         self._sched_ref = ctypes.byref(self.sched.struct)
         self._plan_ref = ctypes.byref(self.plan.struct)
 
+    def set_fused(self, enable: bool) -> None:
+        """Single-launch path (gather + synthesis + plan inside the exec
+        kernel, n <= 6) on/off; off by default (not faster on B200)."""
+        _lib.check_rc(_lib.load().fast_comm_set_fused(self._ptr, 1 if enable else 0), "set_fused")
+
     def close(self) -> None:
         if getattr(self, "_ptr", None):
             _lib.load().fast_comm_destroy(self._ptr)

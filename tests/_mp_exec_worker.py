@@ -46,7 +46,8 @@ def main() -> int:
         cap = max(int(max(c.sum(0).max(), c.sum(1).max())) for c in cases) + 4096
         comm = FastComm(Topology(n, m), recv_bytes=cap, staging_bytes=2 * cap + (1 << 20),
                         blocks=16, chunk_bytes=128 * 1024)
-        for ci, D in enumerate(cases):
+        for ci, D in enumerate(cases + cases):
+            comm.set_fused(ci < len(cases))  # fused single launch, then multi-launch
             sends_np = [payload(g, int(D[g].sum()) + 16) for g in range(world)]
             send = torch.from_numpy(sends_np[rank]).cuda()
             recv = comm.alltoallv(send, torch.from_numpy(D[rank].copy()).cuda())

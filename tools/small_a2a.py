@@ -13,15 +13,20 @@ send = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
 row = torch.from_numpy(D[rank].copy()).cuda()
 for _ in range(20): comm.alltoallv(send, row)
 torch.cuda.synchronize(); dist.barrier()
-t = time.perf_counter()
-for _ in range(200): comm.alltoallv(send, row)
-torch.cuda.synchronize()
-host_us = (time.perf_counter() - t) / 200 * 1e6
-a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-a.record()
-for _ in range(200): comm.alltoallv(send, row)
-b.record(); torch.cuda.synchronize()
-if rank == 0: print(f"per call: wall {host_us:.1f} us, events {a.elapsed_time(b)/200*1e3:.1f} us", flush=True)
+for fused in (True, False):
+    comm.set_fused(fused)
+    for _ in range(20): comm.alltoallv(send, row)
+    torch.cuda.synchronize(); dist.barrier()
+    t = time.perf_counter()
+    for _ in range(200): comm.alltoallv(send, row)
+    torch.cuda.synchronize()
+    host_us = (time.perf_counter() - t) / 200 * 1e6
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(200): comm.alltoallv(send, row)
+    b.record(); torch.cuda.synchronize()
+    comm.check()
+    if rank == 0: print(f"per call (fused={fused}): wall {host_us:.1f} us, events {a.elapsed_time(b)/200*1e3:.1f} us", flush=True)
 comm.close(); dist.destroy_process_group()
 
 # ---- per-stage device breakdown (events between the enqueued stages) ----
@@ -52,4 +57,21 @@ for it in range(120):
 if rank == 0:
     a = acc / 100 * 1e3
     print(f"stages us: gather {a[0]:.1f}  synth {a[1]:.1f}  plan {a[2]:.1f}  exec {a[3]:.1f}  total {a[4]:.1f}", flush=True)
+comm.close(); dist.destroy_process_group()
+
+# ---- fused prologue stamps (globaltimer, ns) ----
+dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
+comm = FastComm(Topology(2, world // 2), recv_bytes=1 << 20, staging_bytes=1 << 20)
+acc = np.zeros(7); cnt = 0
+for it in range(200):
+    comm.alltoallv(send, row, record_timeline=True)
+    if it >= 50 and it % 5 == 0:
+        t = comm.timeline.cpu().numpy()
+        # [5] start, [6] gathered, [7] balanced, [258] decomposed, [0] plan done/barrier start, [1] GO, [3] own ops done, [4] recv complete
+        pts = [t[5], t[6], t[7], t[258], t[0], t[3], t[4]]
+        acc += np.diff(np.array(pts + [pts[-1]], dtype=np.float64))
+        cnt += 1
+if rank == 0:
+    a = acc / cnt / 1e3
+    print(f"fused us: gather {a[0]:.1f} balance {a[1]:.1f} decompose {a[2]:.1f} plan {a[3]:.1f} exec-own {a[4]:.1f} recv-wait {a[5]:.1f}", flush=True)
 comm.close(); dist.destroy_process_group()
