@@ -302,6 +302,20 @@ int fast_moe_pack(const void *tokens, int T, int k, int64_t row_bytes,
 int fast_moe_unpack_self(const int64_t *D, const int64_t *self_bytes, int G,
                          int rank, const void *send, void *recv, void *stream);
 
+/* Combine (the second alltoallv of an MoE layer,
+ * PAPER.md:120): after the reverse FAST alltoallv (counts = column `rank` of
+ * the forward D, self kept local), out[t] = sum_j weights[t][j] * row(t, j)
+ * over token t's k experts, bf16 rows, fp32 round-to-nearest multiply/add in
+ * j order, bf16 RNE result.  Dfwd: the forward call's gathered D (zero
+ * diagonal); expert_out: the expert output in the forward receive layout;
+ * comb_recv: the reverse call's receive buffer.  topk/pos/workspace/seg_rows
+ * are the forward route's. */
+int fast_moe_combine(const void *comb_recv, const void *expert_out,
+                     const int64_t *Dfwd, int G, int rank, int T, int k,
+                     int64_t row_bytes, const int32_t *topk, const int32_t *pos,
+                     const void *workspace, int E, const int64_t *seg_rows,
+                     const float *weights, void *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

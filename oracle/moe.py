@@ -66,3 +66,32 @@ def expert_inputs(tokens: list[np.ndarray], topks: list[np.ndarray], E: int) -> 
             parts.append(sends[s][seg[h]:seg[h] + counts[h]])
         out.append(np.concatenate(parts))
     return out
+
+
+def bf16_to_f32(u16: np.ndarray) -> np.ndarray:
+    return (u16.astype(np.uint32) << np.uint32(16)).view(np.float32)
+
+
+def f32_to_bf16(f: np.ndarray) -> np.ndarray:
+    """Round-to-nearest-even (finite inputs)."""
+    b = f.astype(np.float32).view(np.uint32)
+    return ((b + np.uint32(0x7FFF) + ((b >> np.uint32(16)) & np.uint32(1))) >> np.uint32(16)).astype(np.uint16)
+
+
+def combine(tokens_bf16: list[np.ndarray], topks: list[np.ndarray], weights: list[np.ndarray],
+            expert_scale) -> list[np.ndarray]:
+    """out[t] = bf16( sum_j fl32(w[t,j] * x_j) ) accumulated left to right in
+    float32 (IEEE round-to-nearest per op), x_j = expert e_j's output for
+    token t = token * expert_scale(e_j) (exact power-of-two scaling)."""
+    outs = []
+    for s in range(len(tokens_bf16)):
+        x = bf16_to_f32(tokens_bf16[s])  # [T, H]
+        tk, w = topks[s], weights[s].astype(np.float32)
+        acc = None
+        for j in range(tk.shape[1]):
+            scale = np.array([expert_scale(int(e)) for e in tk[:, j]], np.float32)[:, None]
+            xj = (x * scale).astype(np.float32)
+            p = (w[:, j:j + 1] * xj).astype(np.float32)
+            acc = p if acc is None else (acc + p).astype(np.float32)
+        outs.append(f32_to_bf16(acc))
+    return outs

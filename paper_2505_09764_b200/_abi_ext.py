@@ -45,4 +45,5 @@ SIGNATURES: list[tuple[str, object, list]] = [
     ("fast_moe_route", I, [V, I, I, I, I64, V, V, V, V, V, V]),
     ("fast_moe_pack", I, [V, I, I, I64, V, V, V, I, V, V, V]),
     ("fast_moe_unpack_self", I, [V, V, I, I, V, V, V]),
+    ("fast_moe_combine", I, [V, V, V, I, I, I, I, I64, V, V, V, I, V, V, V, V]),
 ]

@@ -18,6 +18,7 @@
 //                          gap the executor leaves at the self slot of the
 //                          receive buffer, which then IS the expert input
 //                          (source-major, like all_to_all_single)
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -187,6 +188,77 @@ __global__ void moe_unpack_self_kernel(const int64_t* __restrict__ D,
   }
 }
 
+// Combine (the reverse alltoallv's receive side): token t's output is
+// sum_j w[t][j] * row(t, j) over its k experts, in j order with explicit
+// round-to-nearest fp32 multiply and add (no FMA contraction, so the numpy
+// oracle reproduces it bit for bit), then bf16 round-to-nearest-even.
+// row(t, j) of expert e sits at row seg_rows[e] + blkbase + pos of the
+// combine receive buffer (segments by expert, forward pack order); the own
+// expert's rows were never sent and are read from the expert output buffer.
+__device__ __forceinline__ void bf16x8_to_f32(const uint4 v, float (&f)[8]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(256)
+    moe_combine_kernel(const uint8_t* __restrict__ comb_recv,
+                       const uint8_t* __restrict__ expert_out, const int64_t* __restrict__ Dfwd,
+                       int G, int me, int T, int64_t row_vec, const int32_t* __restrict__ topk,
+                       const int32_t* __restrict__ pos, const int32_t* __restrict__ blkbase,
+                       int E, const int64_t* __restrict__ seg_rows,
+                       const float* __restrict__ weights, uint4* __restrict__ out) {
+  __shared__ int64_t s_self_off;
+  if (threadIdx.x == 0) {
+    int64_t o = 0;  // self segment of the expert output (forward recv layout)
+    for (int g = 0; g < me; ++g) o += Dfwd[(int64_t)g * G + me];
+    s_self_off = o;
+  }
+  __syncthreads();
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int64_t RB = row_vec * 16;
+  for (int t = warp; t < T; t += nwarps) {
+    const uint4* src[K];
+    float w[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int i = t * K + j;
+      const int e = topk[i];
+      const int64_t r = blkbase[(int64_t)(i / kRouteThreads) * E + e] + pos[i];
+      src[j] = (e == me)
+                   ? reinterpret_cast<const uint4*>(expert_out + s_self_off + r * RB)
+                   : reinterpret_cast<const uint4*>(comb_recv + (seg_rows[e] + r) * RB);
+      w[j] = weights[i];
+    }
+    for (int64_t v = lane; v < row_vec; v += 32) {
+      float acc[8];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        float x[8];
+        bf16x8_to_f32(ldg_nc(src[j] + v), x);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float p = __fmul_rn(w[j], x[q]);
+          acc[q] = j == 0 ? p : __fadd_rn(acc[q], p);
+        }
+      }
+      uint32_t o[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const __nv_bfloat162 h = __floats2bfloat162_rn(acc[2 * q], acc[2 * q + 1]);
+        o[q] = *reinterpret_cast<const uint32_t*>(&h);
+      }
+      out[(int64_t)t * row_vec + v] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
 int sm_count() {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -260,6 +332,32 @@ int fast_moe_unpack_self(const int64_t* D, const int64_t* self_bytes, int G, int
     return FAST_EVALIDATION;
   moe_unpack_self_kernel<<<2 * sm_count(), 512, 0, (cudaStream_t)stream>>>(
       D, self_bytes, G, rank, (const uint8_t*)send, (uint8_t*)recv);
+  return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
+}
+
+int fast_moe_combine(const void* comb_recv, const void* expert_out, const int64_t* Dfwd, int G,
+                     int rank, int T, int k, int64_t row_bytes, const int32_t* topk,
+                     const int32_t* pos, const void* workspace, int E, const int64_t* seg_rows,
+                     const float* weights, void* out, void* stream) {
+  if (T < 0 || (k != 1 && k != 2 && k != 4 && k != 8) || row_bytes <= 0 || (row_bytes & 15) ||
+      !comb_recv || !expert_out || !Dfwd || !topk || !pos || !workspace || !seg_rows ||
+      !weights || !out || rank < 0 || rank >= G || ((uintptr_t)out & 15))
+    return FAST_EVALIDATION;
+  if (T == 0) return FAST_OK;
+  int blocks = (int)(((int64_t)T * 32 + 255) / 256);
+  if (blocks > 8 * sm_count()) blocks = 8 * sm_count();
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t rv = row_bytes / 16;
+  const uint8_t* cr = (const uint8_t*)comb_recv;
+  const uint8_t* eo = (const uint8_t*)expert_out;
+  const int32_t* bb = (const int32_t*)workspace;
+  uint4* o = (uint4*)out;
+  switch (k) {
+    case 1: moe_combine_kernel<1><<<blocks, 256, 0, s>>>(cr, eo, Dfwd, G, rank, T, rv, topk, pos, bb, E, seg_rows, weights, o); break;
+    case 2: moe_combine_kernel<2><<<blocks, 256, 0, s>>>(cr, eo, Dfwd, G, rank, T, rv, topk, pos, bb, E, seg_rows, weights, o); break;
+    case 4: moe_combine_kernel<4><<<blocks, 256, 0, s>>>(cr, eo, Dfwd, G, rank, T, rv, topk, pos, bb, E, seg_rows, weights, o); break;
+    default: moe_combine_kernel<8><<<blocks, 256, 0, s>>>(cr, eo, Dfwd, G, rank, T, rv, topk, pos, bb, E, seg_rows, weights, o); break;
+  }
   return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
 }
 

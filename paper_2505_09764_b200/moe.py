@@ -108,4 +108,41 @@ class MoEDispatch:
         self.route(seed, stream)
         self.pack(tokens, stream)
         self.comm.alltoallv(self.send, self.demand_row, stream=stream)
+        self.remember_forward(self.comm.demand(), self.comm.self_sizes())
         return self.unpack(stream)
+
+    def remember_forward(self, D: torch.Tensor, self_sizes: torch.Tensor) -> None:
+        """Keep the forward call's demand matrix: the combine sends column
+        `rank` of it back (D^T), self segment kept local."""
+        r = self.comm.rank
+        self.Dfwd = D.clone()
+        self.comb_counts = D[:, r].clone()
+        self.comb_counts[r] = self_sizes[r]
+
+    def combine_rows(self, comb_recv: torch.Tensor, expert_out: torch.Tensor,
+                     weights: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
+        """Weighted un-permute of the combine receive buffer into token order
+        (fast_moe_combine); `out` is [T, row_bytes/2] bf16."""
+        lib = _lib.load()
+        P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        if weights.dtype != torch.float32 or weights.numel() != self.T * self.k:
+            raise ValidationError("weights must be float32 [T, k]")
+        if out.dtype != torch.bfloat16 or out.numel() * 2 != self.T * self.row_bytes:
+            raise ValidationError("out must be bf16 [T, row_bytes/2]")
+        _lib.check_rc(lib.fast_moe_combine(P(comb_recv), P(expert_out), P(self.Dfwd),
+                                           self.comm.world, self.comm.rank, self.T, self.k,
+                                           self.row_bytes, P(self.topk), P(self.pos), P(self.ws),
+                                           self.E, P(self.seg_rows), P(weights.contiguous()),
+                                           P(out), _stream_handle(stream)), "fast_moe_combine")
+        return out
+
+    def combine(self, expert_out: torch.Tensor, weights: torch.Tensor, out: torch.Tensor,
+                stream=None) -> torch.Tensor:
+        """Reverse FAST alltoallv of the expert outputs (forward receive
+        layout; must not alias the communicator's receive region) and the
+        weighted top-k combine back into token order."""
+        if expert_out.data_ptr() == self.comm.recv.data_ptr():
+            raise ValidationError("expert_out must not alias the receive region")
+        recv = self.comm.alltoallv(expert_out.view(torch.uint8).reshape(-1), self.comb_counts,
+                                   stream=stream)
+        return self.combine_rows(recv, expert_out, weights, out, stream)

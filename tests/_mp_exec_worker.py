@@ -84,7 +84,9 @@ def main() -> int:
         mcomm = FastComm(Topology(n, m), recv_bytes=2 * T * RB * 3, staging_bytes=2 * T * RB * 3,
                          blocks=64)
         disp = MoEDispatch(mcomm, T, RB)
-        toks = [payload(500 + s, T * RB).reshape(T, RB) for s in range(world)]
+        rngt = np.random.default_rng(500)
+        toks = [(rngt.standard_normal((T, RB // 2), dtype=np.float32).view(np.uint32) >> 16)
+                .astype(np.uint16).view(np.uint8).reshape(T, RB) for _ in range(world)]
         recv = disp.dispatch(torch.from_numpy(toks[rank]).cuda(), seed=1)
         torch.cuda.synchronize()
         mcomm.check()
@@ -95,6 +97,24 @@ def main() -> int:
         if not np.array_equal(got, want):
             print(f"[rank {rank}] MoE expert input mismatch (n={n}, m={m})", flush=True)
             ok = False
+        # combine: experts scale by 2^rank (exact), reverse FAST alltoallv, weighted sum
+        n_in = want.size
+        expert_out = torch.zeros(2 * T * RB * 3, dtype=torch.uint8, device="cuda")
+        xb = (recv[:n_in].view(torch.bfloat16) * (2.0 ** rank)).view(torch.uint8)
+        expert_out[:n_in].copy_(xb)
+        wts = [np.random.default_rng(900 + s_).random((T, 2), dtype=np.float32) for s_ in range(world)]
+        out = torch.empty(T, RB // 2, dtype=torch.bfloat16, device="cuda")
+        disp.combine(expert_out, torch.from_numpy(wts[rank]).cuda(), out)
+        torch.cuda.synchronize()
+        mcomm.check()
+        toks16 = [t.view(np.uint16) for t in toks]  # payload bytes read as bf16 (finite: checked)
+        finite = all(np.isfinite(moe_oracle.bf16_to_f32(t)).all() for t in toks16)
+        if finite:
+            wantc = moe_oracle.combine(toks16, topks, wts, lambda e: 2.0 ** e)[rank]
+            gotc = out.cpu().view(torch.int16).numpy().view(np.uint16)
+            if not np.array_equal(gotc, wantc):
+                print(f"[rank {rank}] MoE combine mismatch (n={n}, m={m})", flush=True)
+                ok = False
         mcomm.close()
         comm.close()
         dist.barrier()

@@ -76,3 +76,58 @@ def test_moe_dispatch_group_mode_matches_oracle():
         got = recvs[h][:n].cpu().numpy().reshape(-1, RB)
         assert np.array_equal(got, want[h]), h
     group.close()
+
+
+@pytest.mark.gpu
+def test_moe_combine_group_mode_matches_oracle():
+    """dispatch -> experts (x * 2^e, exact) -> reverse FAST alltoallv (D^T) ->
+    weighted combine: bit-exact vs the numpy oracle."""
+    from paper_2505_09764_b200 import Topology
+    from paper_2505_09764_b200.executor import GroupComm, GroupRank
+    from paper_2505_09764_b200.moe import MoEDispatch
+
+    G, T, H, seed = 8, 2000, 512, 4
+    RB = 2 * H
+    gen = torch.Generator().manual_seed(0)
+    toks = [torch.randn(T, H, generator=gen).to(torch.bfloat16) for _ in range(G)]
+    toks_u16 = [t.view(torch.int16).numpy().view(np.uint16) for t in toks]
+    weights = [torch.rand(T, 2, generator=gen, dtype=torch.float32) for _ in range(G)]
+    cap = 2 * T * RB * 4
+    group = GroupComm(Topology(2, 4), recv_bytes=cap, staging_bytes=cap, blocks=8)
+    disps = []
+    for s in range(G):
+        d = MoEDispatch(GroupRank(group, s), T, RB)
+        d.route(seed)
+        d.pack(toks[s].cuda())
+        disps.append(d)
+    Dfull = torch.stack([d.demand_row for d in disps])
+    selfb = torch.diagonal(Dfull).clone()
+    D = Dfull.clone()
+    D.fill_diagonal_(0)
+    recvs = group.alltoallv([d.send for d in disps], D, self_bytes=selfb)
+    expert_out = []
+    for h, d in enumerate(disps):
+        d.unpack(D=D, self_sizes=selfb, recv=recvs[h])
+        d.remember_forward(D, selfb)
+        n_in = int(Dfull[:, h].sum().item())
+        x = recvs[h][:n_in].view(torch.bfloat16) * (2.0 ** h)  # expert h (exact)
+        buf = torch.empty(cap, dtype=torch.uint8, device="cuda")
+        buf[:n_in].copy_(x.view(torch.uint8))
+        expert_out.append(buf)
+    # reverse alltoallv: rank h sends column h of the forward D back (D^T)
+    Dt = D.t().contiguous()
+    comb = group.alltoallv(expert_out, Dt, self_bytes=selfb)
+    outs = []
+    for s, d in enumerate(disps):
+        o = torch.empty(T, H, dtype=torch.bfloat16, device="cuda")
+        d.combine_rows(comb[s], expert_out[s], weights[s].cuda(), o)
+        outs.append(o)
+    torch.cuda.synchronize()
+    group.check()
+    thr, thr2 = gating_thresholds(G)
+    topks = [moe_oracle.gate(seed, s, T, thr, thr2) for s in range(G)]
+    want = moe_oracle.combine(toks_u16, topks, [w.numpy() for w in weights], lambda e: 2.0 ** e)
+    for s in range(G):
+        got = outs[s].cpu().view(torch.int16).numpy().view(np.uint16)
+        assert np.array_equal(got, want[s]), s
+    group.close()
