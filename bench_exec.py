@@ -327,6 +327,25 @@ def run_moe(args) -> dict | None:
     nms = torch.tensor([n0.elapsed_time(n1) / args.steps], device="cuda")
     dist.all_reduce(nms, op=dist.ReduceOp.MAX)
     nms = float(nms.item())
+    # combine (the second alltoallv of the layer): identity experts
+    expert_out = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    expert_out.copy_(recv[:cap])
+    wts = torch.rand(T, 2, dtype=torch.float32, device="cuda")
+    comb_out = torch.empty(T, hidden, dtype=torch.bfloat16, device="cuda")
+    for _ in range(args.warmup):
+        disp.combine(expert_out, wts, comb_out)
+    torch.cuda.synchronize()
+    dist.barrier()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record(stream)
+    for _ in range(args.steps):
+        disp.combine(expert_out, wts, comb_out)
+    c1.record(stream)
+    torch.cuda.synchronize()
+    comm.check()
+    cms = torch.tensor([c0.elapsed_time(c1) / args.steps], device="cuda")
+    dist.all_reduce(cms, op=dist.ReduceOp.MAX)
+    cms = float(cms.item())
     D = comm.demand().cpu().numpy()
     cross = int(D.sum())
     bn = int(max(D.sum(0).max(), D.sum(1).max()))
@@ -345,6 +364,8 @@ def run_moe(args) -> dict | None:
                           "bottleneck_gpu_bytes": bn},
                "t_roof_us": round(bn / (PEER_GBS * 1e9) * 1e6, 1),
                "frac_of_alltoallv_roofline": round(bn / (PEER_GBS * 1e9) / (ms * 1e-3), 4),
+               "combine_ms": round(cms, 4),
+               "layer_dispatch_plus_combine_ms": round(ms + cms, 4),
                "nccl_path": {"ms": round(nms, 4),
                              "value": round(T * world / (nms * 1e-3), 1), "unit": "tokens/s",
                              "what": "same route+pack kernels + NCCL all_to_all_single"},

@@ -1,0 +1,145 @@
+"""Host-side logic of the multi-GPU path, world_size 2 on CPU (gloo).
+
+* count all-gather semantics: every rank assembles the same D (zero
+  diagonal) and self-size vector from the per-rank rows;
+* every rank independently derives the identical schedule and plan from
+  the gathered D (the paper's "same schedule on every GPU, no exchange",
+  PAPER.md:615);
+* message-passing execution of the plan: each rank runs only its own ops
+  phase by phase and ships the written bytes to their owners; every
+  receive buffer equals the direct alltoallv (self slot left as a gap);
+* all_to_all_fast's split/offset arithmetic against gloo's
+  all_to_all_single, with a stand-in transport.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import REPO
+
+WORLD = 2
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+class _GlooComm:
+    """Stand-in transport with FastComm's alltoallv contract (receive layout
+    of all_to_all_single with a gap at the self slot)."""
+
+    def __init__(self):
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+
+    def alltoallv(self, send: torch.Tensor, counts: torch.Tensor) -> torch.Tensor:
+        rows = [torch.zeros(self.world, dtype=torch.int64) for _ in range(self.world)]
+        dist.all_gather(rows, counts.to(torch.int64))
+        D = torch.stack(rows)
+        out_splits = D[:, self.rank].tolist()
+        recv = torch.empty(int(sum(out_splits)), dtype=torch.uint8)
+        dist.all_to_all_single(recv, send[: int(counts.sum())], out_splits, counts.tolist())
+        lo = int(sum(out_splits[: self.rank]))
+        recv[lo:lo + out_splits[self.rank]] = 0  # the self slot is a gap
+        return recv
+
+
+def _worker(rank: int, port: int, errq):
+    import sys
+
+    sys.path.insert(0, REPO)
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+        from oracle import oracle
+        from oracle.alltoallv import direct_alltoallv, payload
+        from paper_2505_09764_b200 import workloads
+        from paper_2505_09764_b200.executor import (BUF_RECV, BUF_SEND, all_to_all_fast,
+                                                    plan_compile_host)
+        from paper_2505_09764_b200.schedule import PackedSchedule
+
+        n, m = 2, 1
+        G = n * m
+        D = workloads.zipf_sizes(11, G, 1.2, 200_003)
+        selfb = np.array([777, 1234], dtype=np.int64)
+        Dfull = D + np.diag(selfb)
+        # 1. count all-gather (mirrors gather_demand_kernel's layout)
+        rows = [torch.zeros(G, dtype=torch.int64) for _ in range(G)]
+        dist.all_gather(rows, torch.from_numpy(Dfull[rank].copy()))
+        Dg = torch.stack(rows).numpy()
+        D0 = Dg.copy()
+        np.fill_diagonal(D0, 0)
+        assert np.array_equal(D0, D) and np.array_equal(np.diagonal(Dg), selfb)
+        # 2. schedule + plan on every rank, identical everywhere
+        out = oracle.synthesize_batch(D0, n, m)
+        p = PackedSchedule(**oracle.packed_fields(out, 0, n, m))
+        cap = int(Dfull.sum(axis=0).max()) + 64
+        ops, _, st = plan_compile_host(D0, n, m, p.stage_order, p.stage_perm, p.stage_bytes,
+                                       cap, cap, send_self=selfb, chunk=4096)
+        assert st == 0
+        allops = [None] * G
+        dist.all_gather_object(allops, ops.tobytes())
+        assert all(x == allops[0] for x in allops)
+        # 3. message passing: each rank executes only its own ops, per phase
+        send = payload(rank, int(Dfull[rank].sum()))
+        recv = np.zeros(cap, np.uint8)
+        stg = np.zeros(cap + 64, np.uint8)
+        for ph in range(4):
+            msgs = []
+            for o in ops[(ops["phase"] == ph) & (ops["exec_rank"] == rank)]:
+                src = send if o["src_buf"] == BUF_SEND else stg
+                so, ln = int(o["src_off"]), int(o["len"])
+                msgs.append((int(o["dst_rank"]), int(o["dst_buf"]), int(o["dst_off"]),
+                             src[so:so + ln].tobytes()))
+            got = [None] * G
+            dist.all_gather_object(got, msgs)
+            for lst in got:
+                for dst, buf, off, data in lst:
+                    if dst != rank:
+                        continue
+                    arr = np.frombuffer(data, np.uint8)
+                    (recv if buf == BUF_RECV else stg)[off:off + len(arr)] = arr
+        full = direct_alltoallv([payload(g, int(Dfull[g].sum())) for g in range(G)], Dfull)[rank]
+        lo = int(Dfull[:rank, rank].sum())
+        hi = lo + int(selfb[rank])
+        assert np.array_equal(recv[:lo], full[:lo])
+        assert np.array_equal(recv[hi:len(full)], full[hi:])
+        # 4. all_to_all_fast offset arithmetic vs all_to_all_single
+        splits = np.array([[3, 5], [4, 2]])
+        x = torch.arange(int(splits[rank].sum()) * 6, dtype=torch.int32).reshape(-1, 6) + 1000 * rank
+        y_fast = torch.zeros(int(splits[:, rank].sum()), 6, dtype=torch.int32)
+        y_ref = torch.zeros_like(y_fast)
+        all_to_all_fast(y_fast, x, splits[:, rank].tolist(), splits[rank].tolist(), comm=_GlooComm())
+        dist.all_to_all_single(y_ref, x, splits[:, rank].tolist(), splits[rank].tolist())
+        assert torch.equal(y_fast, y_ref)
+        dist.destroy_process_group()
+    except Exception as exc:  # pragma: no cover - reported by the parent
+        import traceback
+
+        errq.put(f"rank {rank}: {exc!r}\n{traceback.format_exc()}")
+        raise
+
+
+def test_multi_rank_host_logic_gloo():
+    ctx = mp.get_context("spawn")
+    errq = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, port, errq)) for r in range(WORLD)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=300)
+    errs = []
+    while not errq.empty():
+        errs.append(errq.get())
+    assert not errs, "\n".join(errs)
+    assert all(pr.exitcode == 0 for pr in procs), [pr.exitcode for pr in procs]
