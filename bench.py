@@ -182,44 +182,31 @@ def bench_synth(args) -> dict:
                 "note": "decompose is a dependent chain of <= n^2-2n+2 peels per matrix "
                         "(latency-bound); balance is the HBM-bound kernel"}
 
-    # ---- e2e: host (pinned) D -> device -> synth -> packed schedule -> host
+    # ---- e2e: host (pinned) D -> device -> synth -> packed schedule -> host,
+    # through synthesize_host_batch (chunked, copies overlapped with kernels)
     e2e = None
     if not args.no_e2e:
         Dh = torch.empty(D.shape, dtype=D.dtype, pin_memory=True)
         Dh.copy_(D)
-        outs = [getattr(bufs, k) for k in ("balanced", "server", "move_count", "moves",
-                                           "common_sum", "aux", "n_raw", "stage_weight",
-                                           "stage_perm", "stage_bytes", "n_stages",
-                                           "stage_order", "status")]
-        hosts = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in outs]
-        Dd = torch.empty_like(D)
-        h2d = Dh.numel() * 8
-        d2h = sum(h.numel() * h.element_size() for h in hosts)
-
-        def e2e_step():
-            Dd.copy_(Dh, non_blocking=True)
-            rc = lib.fast_synth_batch(ctypes.c_void_p(Dd.data_ptr()), B, n, m,
-                                      ctypes.byref(bufs.struct), sh)
-            _lib.check_rc(rc, "fast_synth_batch")
-            for h, o in zip(hosts, outs):
-                h.copy_(o, non_blocking=True)
-
-        for _ in range(min(args.warmup, 1) or 1):
-            e2e_step()
-        torch.cuda.synchronize()
+        hs = synth.HostSchedules(B, n, m)
+        del bufs
+        torch.cuda.empty_cache()
+        synth.synthesize_host_batch(Dh, n, m, hs, chunk=args.e2e_chunk)  # warm-up
         steps = max(1, min(args.steps, 3))
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(steps):
-            e2e_step()
-        e1.record(stream)
         torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1) / steps
+        t0h = time.perf_counter()
+        for _ in range(steps):
+            synth.synthesize_host_batch(Dh, n, m, hs, chunk=args.e2e_chunk)
+        ems = (time.perf_counter() - t0h) * 1e3 / steps
+        if int(hs.status.abs().max()) != 0:
+            raise RuntimeError("e2e synthesis reported failures")
         e2e = {"value": round(B / (ems * 1e-3), 3), "unit": "matrices/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "h2d_bytes_per_step": int(Dh.numel() * 8), "d2h_bytes_per_step": int(hs.nbytes()),
                "ms_per_step": round(ems, 3), "steps": steps,
-               "path": "C-ABI fast_synth_batch with pinned host buffers"}
-        del Dh, hosts, Dd
+               "path": f"synthesize_host_batch (C-ABI fast_synth_batch per {args.e2e_chunk}-matrix "
+                       "chunk, pinned host buffers, H2D/kernels/D2H overlapped; wall clock "
+                       "incl. the final host sync)"}
+        del Dh, hs
 
     cpu = None
     if not args.no_cpu_baseline:
@@ -363,6 +350,7 @@ def main() -> None:
     ap.add_argument("--hidden", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunk", type=int, default=125)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 

@@ -223,3 +223,71 @@ def decompose(embedded: np.ndarray) -> list[PermutationStage]:
     p = _decompose_packed(e.astype(np.int64), _lib.FAST_DEC_DOUBLY_STOCHASTIC)
     _raise_status(p.status, "decompose")
     return list(p.raw_stages())
+
+
+_PACKED_FIELDS = ("balanced", "server", "move_count", "moves", "common_sum", "aux", "n_raw",
+                  "stage_weight", "stage_perm", "stage_bytes", "n_stages", "stage_order", "status")
+
+
+class HostSchedules:
+    """Pinned host copy of a batch's packed schedules (same layout as
+    SynthBuffers), the output of synthesize_host_batch."""
+
+    def __init__(self, B: int, n: int, m: int):
+        like = SynthBuffers.__new__(SynthBuffers)  # shapes only
+        G, T, S, K = n * m, n * (n - 1), max(m - 1, 1), stage_cap(n)
+        shapes = {"balanced": ((B, G, G), torch.int64), "server": ((B, n, n), torch.int64),
+                  "move_count": ((B, T), torch.int32), "moves": ((B, T, S, 2), torch.int64),
+                  "common_sum": ((B,), torch.int64), "aux": ((B, n, n), torch.int64),
+                  "n_raw": ((B,), torch.int32), "stage_weight": ((B, K), torch.int64),
+                  "stage_perm": ((B, K, n), torch.uint8), "stage_bytes": ((B, K, n), torch.int64),
+                  "n_stages": ((B,), torch.int32), "stage_order": ((B, K), torch.int32),
+                  "status": ((B,), torch.int32)}
+        del like
+        self.B, self.n, self.m = B, n, m
+        for k, (shape, dt) in shapes.items():
+            setattr(self, k, torch.empty(shape, dtype=dt, pin_memory=True))
+
+    def nbytes(self) -> int:
+        return sum(getattr(self, k).numel() * getattr(self, k).element_size() for k in _PACKED_FIELDS)
+
+
+def synthesize_host_batch(D_host: torch.Tensor, n: int, m: int, out: HostSchedules | None = None,
+                          chunk: int = 125, device=None, _cache: dict = {}) -> HostSchedules:
+    """synthesize_fast over a batch held in (pinned) HOST memory.
+
+    The batch is split into chunks, each on its own stream with its own
+    device buffers: chunk i's H2D, synthesis and D2H are stream-ordered, the
+    chunks are independent, so the copy engines stream the inputs and
+    results while every chunk's (latency-bound) decomposition runs
+    concurrently on the SMs.  Returns after the last D2H."""
+    dev = device or _device()
+    if D_host.device.type != "cpu" or D_host.dtype != torch.int64 or D_host.dim() != 3:
+        raise ValidationError("D_host must be a CPU int64 tensor [B, G, G]")
+    B = D_host.shape[0]
+    out = out or HostSchedules(B, n, m)
+    lib = _lib.load()
+    C = max(1, min(chunk, B))
+    starts = list(range(0, B, C))
+    key = (str(dev), B, n, m, C)
+    if key not in _cache:  # device buffers and streams are reused across calls
+        _cache.clear()
+        _cache[key] = ([SynthBuffers(min(C, B - b0), n, m, dev) for b0 in starts],
+                       [torch.empty((min(C, B - b0), n * m, n * m), dtype=torch.int64, device=dev)
+                        for b0 in starts],
+                       [torch.cuda.Stream(dev) for _ in starts])
+    bufs, dins, streams = _cache[key]
+    cur = torch.cuda.current_stream(dev)
+    for i, b0 in enumerate(starts):
+        st, nb = streams[i], dins[i].shape[0]
+        st.wait_stream(cur)
+        with torch.cuda.stream(st):
+            dins[i].copy_(D_host[b0:b0 + nb], non_blocking=True)
+            rc = lib.fast_synth_batch(ctypes.c_void_p(dins[i].data_ptr()), nb, n, m,
+                                      ctypes.byref(bufs[i].struct), ctypes.c_void_p(st.cuda_stream))
+            _lib.check_rc(rc, "fast_synth_batch")
+            for f in _PACKED_FIELDS:
+                getattr(out, f)[b0:b0 + nb].copy_(getattr(bufs[i], f), non_blocking=True)
+    for st in streams:
+        st.synchronize()
+    return out
