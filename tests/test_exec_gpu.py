@@ -103,3 +103,42 @@ def test_group_exec_reports_small_buffers():
     with pytest.raises(ValidationError):
         comm.check()
     comm.close()
+
+
+def test_group_exec_edge_cases():
+    """Empty traffic, 1-byte and sub-16-byte (misaligned) segments, a single
+    huge segment, and changing traffic across epochs on one communicator."""
+    n, m = 2, 4
+    G = n * m
+    rng = np.random.default_rng(5)
+    cases = [np.zeros((G, G), np.int64)]
+    one = np.zeros((G, G), np.int64)
+    one[3, 6] = 1
+    cases.append(one)
+    tiny = rng.integers(0, 16, (G, G)).astype(np.int64)
+    np.fill_diagonal(tiny, 0)
+    cases.append(tiny)
+    huge = np.zeros((G, G), np.int64)
+    huge[0, 7] = 50_000_017
+    cases.append(huge)
+    odd = rng.integers(1, 70_000, (G, G)).astype(np.int64) * 3 + 1
+    np.fill_diagonal(odd, 0)
+    cases.append(odd)
+    cap = max(int(max(c.sum(0).max(), c.sum(1).max())) for c in cases) + 4096
+    comm = GroupComm(Topology(n, m), recv_bytes=cap, staging_bytes=2 * cap + (1 << 20),
+                     blocks=8, chunk_bytes=64 * 1024)
+    for D in cases + cases[::-1]:
+        _check(comm, D)
+    comm.close()
+
+
+@pytest.mark.parametrize("n,m", [(8, 1), (2, 8)])
+def test_group_exec_wide_partitions(n, m):
+    G = n * m
+    D = workloads.zipf_sizes(7, G, 1.1, 20_000_003)
+    cap = int(max(D.sum(0).max(), D.sum(1).max())) + 4096
+    comm = GroupComm(Topology(n, m), recv_bytes=cap, staging_bytes=2 * cap + (1 << 20),
+                     blocks=max(1, 144 // G), chunk_bytes=64 * 1024)
+    _check(comm, D)
+    _check(comm, workloads.gen_adversarial(Topology(n, m), 1_000_003).sizes)
+    comm.close()
