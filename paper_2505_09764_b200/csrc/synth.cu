@@ -29,7 +29,13 @@
 
 namespace {
 
-constexpr int kBalThreads = 256;
+#ifndef FAST_BAL_THREADS
+#define FAST_BAL_THREADS 128
+#endif
+#ifndef FAST_BAL_STRIP_KB
+#define FAST_BAL_STRIP_KB 16
+#endif
+constexpr int kBalThreads = FAST_BAL_THREADS;
 constexpr int kDecWarps = 4;  // matrices per CTA in decompose_kernel
 
 // Optional section timers (debug builds with -DFAST_DEC_PROFILE only).
@@ -237,7 +243,7 @@ int launch_balance(const int64_t* D, int B, int n, int m,
   const size_t tile_bytes = (size_t)(m * m + 1) * 8;
   // ~32 KiB strips: several CTAs per SM overlap the per-tile sequential
   // balancing of one CTA with the HBM traffic of the others.
-  int J = (int)((32 * 1024) / tile_bytes);
+  int J = (int)((FAST_BAL_STRIP_KB * 1024) / tile_bytes);
   if (J > 64) J = 64;
   if (J > n) J = n;
   if (J < 1) J = 1;  // m >= 45: one 16+ KiB tile per CTA
