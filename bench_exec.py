@@ -85,21 +85,27 @@ def run(args, workload: str) -> dict | None:
     if int(okt.item()) != 0:
         raise RuntimeError("FAST alltoallv result differs from NCCL all_to_all_single")
 
+    # timed: the product call (CUDA-graph replay of gather+synthesis+plan+exec)
     for _ in range(args.warmup):
         comm.alltoallv(send, row)
     torch.cuda.synchronize()
     dist.barrier()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         t0.record(stream)
-        for k in range(args.steps):
-            comm.alltoallv(send, row, exec_events=ev[k])
+        for _ in range(args.steps):
+            comm.alltoallv(send, row)
         t1.record(stream)
         torch.cuda.synchronize()
     comm.check()
     step_ms = t0.elapsed_time(t1) / args.steps
+    # exec kernel alone (same traffic, step-by-step path with events around it)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    for k in range(args.steps):
+        comm.alltoallv(send, row, exec_events=ev[k])
+    torch.cuda.synchronize()
+    comm.check()
     exec_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
     mx = torch.tensor([step_ms, exec_ms], device="cuda")
     dist.all_reduce(mx, op=dist.ReduceOp.MAX)

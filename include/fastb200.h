@@ -193,8 +193,9 @@ int fast_comm_open_peers(fast_comm *c, const void *handles);
 int fast_comm_destroy(fast_comm *c);
 void *fast_comm_recv_ptr(const fast_comm *c);
 void *fast_comm_staging_ptr(const fast_comm *c);
-/* demand-matrix buffer of call `epoch` (double-buffered by parity): G x G
- * int64 with zero diagonal, followed by G int64 self-segment sizes */
+/* demand-matrix buffer of call `epoch` (double-buffered by parity; epoch <= 0:
+ * the fixed slot holding the latest gathered matrix): G x G int64 with zero
+ * diagonal, followed by G int64 self-segment sizes */
 int64_t *fast_comm_demand_ptr(const fast_comm *c, int64_t epoch);
 int64_t fast_comm_recv_capacity(const fast_comm *c);
 int64_t fast_comm_staging_capacity(const fast_comm *c);
@@ -219,7 +220,7 @@ int fast_gather_demand(fast_comm *c, const int64_t *row, int64_t epoch,
  * this proxy complete. */
 int fast_exec(fast_comm *c, const fast_plan *plan, const void *send,
               int64_t epoch, int blocks, int64_t chunk_bytes,
-              int64_t *timeline_ns, void *stream);
+              int64_t *timeline_ns, void *stream); /* epoch 0: device counter */
 /* One-GPU group mode (testing the full protocol on a single device): `world`
  * communicators whose symmetric blocks all live on the current device, and
  * one cooperative launch (grid = blocks x world, all CTAs co-resident) that
@@ -234,8 +235,10 @@ int fast_exec_group(fast_comm *const *comms, int world, const fast_plan *plan,
  * demand all-gather of `counts` (device int64[world], entry `rank` = own
  * segment kept in place), synthesis into `sched` (B = 1), plan compile into
  * `plan`, P2P execution.  The receive buffer (fast_comm_recv_ptr) then holds
- * the all_to_all_single layout with a gap at the self slot.  Replaces the
- * paper's all_to_all_FAST runtime call. */
+ * the all_to_all_single layout with a gap at the self slot.  Every argument
+ * of the enqueued launches is call-invariant (the epoch lives on the
+ * device), so a call can be captured once in a CUDA graph and replayed.
+ * Replaces the paper's all_to_all_FAST runtime call. */
 int fast_alltoallv(fast_comm *c, const void *send, const int64_t *counts, int n,
                    int m, const fast_sched_bufs *sched, const fast_plan *plan,
                    int blocks, int64_t chunk_bytes, int64_t *timeline_ns,

@@ -10,7 +10,7 @@
 //
 // Kernels (all stream-ordered on the caller's stream, no host round trip):
 //   gather_demand_kernel  P2P all-gather of the per-rank demand rows
-//   plan_kernel           plan_compile (plan.cuh) in one device thread
+//   plan_kernel           plan_compile_par (plan_par.cuh), one CTA
 //   exec_kernel           persistent, `blocks` CTAs per rank: entry barrier,
 //                         then the rank's ops in phase order, chunked, each
 //                         chunk a 16-byte-vectorised copy into peer HBM
@@ -28,7 +28,7 @@
 #include <string.h>
 
 #include "fastb200.h"
-#include "plan.cuh"
+#include "plan_par.cuh"
 #include "synth_dev.cuh"
 
 namespace {
@@ -42,6 +42,8 @@ constexpr int CTR_GATHER = 4;   // demand rows landed (monotonic)
 constexpr int CTR_STATUS = 5;   // local error word
 constexpr int CTR_WORK_P = 6;   // local: next producer chunk (reset per call)
 constexpr int CTR_WORK_F = 7;   // local: next forwarder chunk (reset per call)
+constexpr int CTR_EPOCH = 9;    // local: epoch of the current call (device-side
+                                // source of truth, so calls can be graph-captured)
 constexpr int kMaxStages = 256;
 #ifndef FAST_EXEC_THREADS
 #define FAST_EXEC_THREADS 512
@@ -220,12 +222,35 @@ __device__ bool gather_rows(uint8_t* const* peers, const int64_t* row, int64_t e
   return __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
 }
 
+// epoch_in > 0: use it; 0: this call's epoch is the device counter + 1.
+// After the gather the matrix (+ self sizes) is copied into the fixed third
+// slot, so later kernels of the call take call-invariant pointers.
+__global__ void bump_epoch_kernel(uint8_t* me) {
+  volatile uint64_t* ep = reinterpret_cast<volatile uint64_t*>(me) + CTR_EPOCH;
+  *ep = *ep + 1;
+}
+
 __global__ void gather_demand_kernel(uint8_t* const* peers, const int64_t* row,
-                                     int64_t epoch, int rank, int world,
+                                     int64_t epoch_in, int rank, int world,
                                      int64_t demand_off) {
+  __shared__ int64_t s_epoch;
   if (threadIdx.x >= 32) return;
-  if (!gather_rows(peers, row, epoch, rank, world, demand_off) && threadIdx.x == 0)
-    atomicExch(reinterpret_cast<unsigned long long*>(ctr(peers[rank], CTR_STATUS)), 3ull);
+  uint8_t* me = peers[rank];
+  if (threadIdx.x == 0) {
+    volatile uint64_t* ep = reinterpret_cast<volatile uint64_t*>(me) + CTR_EPOCH;
+    const int64_t e = epoch_in > 0 ? epoch_in : (int64_t)*ep + 1;
+    *ep = (uint64_t)e;
+    s_epoch = e;
+  }
+  __syncwarp();
+  const int64_t e = s_epoch;
+  const bool ok = gather_rows(peers, row, e, rank, world, demand_off);
+  if (!ok && threadIdx.x == 0)
+    atomicExch(reinterpret_cast<unsigned long long*>(ctr(me, CTR_STATUS)), 3ull);
+  const int64_t slot = (int64_t)world * world + world;
+  const int64_t* src = reinterpret_cast<const int64_t*>(me + demand_off) + (e & 1) * slot;
+  int64_t* dst = reinterpret_cast<int64_t*>(me + demand_off) + 2 * slot;
+  for (int64_t i = threadIdx.x; i < slot; i += 32) dst[i] = src[i];
 }
 
 __device__ __forceinline__ int64_t nchunks(int64_t len, int64_t chunk) {
@@ -253,10 +278,11 @@ __global__ void __launch_bounds__(kExecThreads) raw_copy_kernel(uint8_t* dst, co
 constexpr int kPlanThreads = 256;
 constexpr size_t kPlanSmemMax = 160 * 1024;
 
+__host__ __device__ inline int plan_stage_cap(int n) { return n * n - 2 * n + 2; }
+
 __host__ __device__ inline size_t plan_smem_bytes(int n, int m) {
-  const int64_t G = (int64_t)n * m, K = (int64_t)n * n - 2 * n + 2;
-  size_t b = (size_t)fastplan::plan_ws_bytes(n, m) + 16;
-  b += (size_t)fastplan::plan_op_capacity(n, m, (int)K) * sizeof(fast_op);  // op buckets
+  const int64_t G = (int64_t)n * m, K = plan_stage_cap(n);
+  size_t b = (size_t)fastplan::par_ws_bytes(n, m, (int)K) + 16;
   b += (size_t)(G * G + G) * 8;        // D + self sizes
   b += (size_t)K * 4 + 16;             // order
   b += (size_t)K * n + 16;             // perm
@@ -264,14 +290,16 @@ __host__ __device__ inline size_t plan_smem_bytes(int n, int m) {
   return (b + 127) & ~(size_t)127;
 }
 
-// Stage the plan inputs + workspace in `psm` (whole CTA), then thread 0
-// walks the plan.  Caller guarantees the synthesis status is OK.
+// Stage the plan inputs + workspace in `psm` (whole CTA) when they fit
+// (`smem_ok`), else run on the global copies and the global workspace; the
+// whole CTA then builds the plan (plan_par.cuh).  Caller guarantees the
+// synthesis status is OK.
 __device__ void plan_cta(fastplan::PlanIn in, fastplan::PlanOut out, char* psm, int smem_ok) {
+  void* ws = out.ws;
   if (smem_ok) {
     const int n = in.n, G = in.n * in.m, K = in.K;
     char* p = psm;
-    char* ws = p; p += ((size_t)fastplan::plan_ws_bytes(in.n, in.m) + 16 + 15) & ~(size_t)15;
-    fast_op* scratch = (fast_op*)p; p += (size_t)in.op_cap * sizeof(fast_op);
+    ws = p; p += ((size_t)fastplan::par_ws_bytes(in.n, in.m, K) + 16 + 15) & ~(size_t)15;
     int64_t* D = (int64_t*)p; p += (size_t)G * G * 8;
     int64_t* ss = (int64_t*)p; p += (size_t)G * 8;
     int32_t* ord = (int32_t*)p; p += ((size_t)K * 4 + 16 + 15) & ~(size_t)15;
@@ -292,16 +320,15 @@ __device__ void plan_cta(fastplan::PlanIn in, fastplan::PlanOut out, char* psm, 
     in.order = ord;
     in.sbytes = sb;
     in.perm = pm;
-    out.ws = ws;
-    out.scratch = scratch;
   }
-  if (threadIdx.x == 0) fastplan::plan_compile(in, out);
+  fastplan::plan_compile_par(in, out, ws);
 }
 
 __global__ void __launch_bounds__(kPlanThreads)
     fast_plan_kernel_dev(fastplan::PlanIn in, fastplan::PlanOut out, const int32_t* n_stages,
                          const int32_t* sched_status, int smem_ok) {
   extern __shared__ __align__(16) char psm[];
+  PLAN_STAMP(9);
   if (*sched_status != FAST_OK) {
     if (threadIdx.x == 0) {
       *out.n_ops = 0;
@@ -309,6 +336,7 @@ __global__ void __launch_bounds__(kPlanThreads)
     }
     return;
   }
+  PLAN_STAMP(0);
   in.n_stages = *n_stages;
   plan_cta(in, out, psm, smem_ok);
 }
@@ -345,6 +373,12 @@ __device__ bool fused_prologue(const FusedArgs& f, uint8_t* const* peers, int ra
   const int n = f.n, m = f.m, G = n * m;
   const int64_t* D = reinterpret_cast<const int64_t*>(peers[rank] + f.demand_off) +
                      (epoch & 1) * ((int64_t)G * G + G);
+  __syncthreads();
+  {  // the fixed slot always holds the latest gathered matrix (+ self sizes)
+    int64_t* fixed = reinterpret_cast<int64_t*>(peers[rank] + f.demand_off) +
+                     2 * ((int64_t)G * G + G);
+    for (int i = tid; i < G * G + G; i += blockDim.x) fixed[i] = D[i];
+  }
   if (tid == 0) *f.sched.status = FAST_OK;
   if (tl && tid == 0) tl[6] = (int64_t)globaltimer();
   __syncthreads();
@@ -424,12 +458,13 @@ __global__ void __launch_bounds__(kExecThreads) exec_kernel(ExecArgs a, FusedArg
   uint8_t* me = a.peers[a.rank];
   uint64_t* status = ctr(me, CTR_STATUS);
   const int tid = threadIdx.x;
-  const uint64_t epoch = (uint64_t)a.epoch;
+  const uint64_t epoch =
+      a.epoch > 0 ? (uint64_t)a.epoch : *reinterpret_cast<volatile uint64_t*>(ctr(me, CTR_EPOCH));
   if (tid == 0) s_fail = 0;
   // fused path: CTA 0 gathers D, synthesises the schedule and compiles the
   // plan before the barrier; the other CTAs wait for GO as usual
   if (FUSED && blockIdx.x == 0) {
-    if (!fused_prologue(f, a.peers, a.rank, a.world, a.epoch, fsm, a.timeline) && tid == 0)
+    if (!fused_prologue(f, a.peers, a.rank, a.world, (int64_t)epoch, fsm, a.timeline) && tid == 0)
       s_fail = 1;
     __syncthreads();
   }
@@ -562,7 +597,9 @@ struct fast_comm {
 extern "C" {
 
 size_t fast_plan_workspace_bytes(int n, int m) {
-  return (size_t)fastplan::plan_ws_bytes(n, m);
+  const int64_t seq = fastplan::plan_ws_bytes(n, m);
+  const int64_t par = fastplan::par_ws_bytes(n, m, plan_stage_cap(n));
+  return (size_t)(seq > par ? seq : par);
 }
 
 int64_t fast_plan_op_capacity(int n, int m) {
@@ -608,6 +645,13 @@ int fast_plan_compile(const int64_t* D, const int64_t* send_self, int n, int m,
       in, out, sched->n_stages, sched->status, smem_ok);
   return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
 }
+
+#ifdef FAST_PLAN_PROFILE
+int fast_debug_plan_prof(long long* out16) {
+  return cudaMemcpyFromSymbol(out16, fastplan::g_plan_prof, 16 * sizeof(long long)) == cudaSuccess
+             ? 0 : FAST_ECUDA;
+}
+#endif
 
 int fast_plan_compile_host(const int64_t* D, const int64_t* send_self, int n, int m,
                            int n_stages, const int32_t* order,
@@ -655,7 +699,7 @@ int fast_comm_create(int rank, int world, int max_gpus_per_row, int64_t recv_byt
   c->recv_bytes = recv_bytes;
   c->staging_bytes = staging_bytes;
   c->demand_off = kFlagBytes;  // counters + per-chunk slot flags
-  c->recv_off = fastplan::align16(c->demand_off + 2 * ((int64_t)world * world + world) * 8 + 256);
+  c->recv_off = fastplan::align16(c->demand_off + 3 * ((int64_t)world * world + world) * 8 + 256);
   c->recv_off = (c->recv_off + 4095) & ~(int64_t)4095;
   c->staging_off = (c->recv_off + recv_bytes + 64 + 4095) & ~(int64_t)4095;
   c->total = (c->staging_off + staging_bytes + 64 + 4095) & ~(int64_t)4095;
@@ -722,8 +766,11 @@ void* fast_comm_recv_ptr(const fast_comm* c) { return c ? c->base + c->recv_off 
 void* fast_comm_staging_ptr(const fast_comm* c) { return c ? c->base + c->staging_off : nullptr; }
 int64_t* fast_comm_demand_ptr(const fast_comm* c, int64_t epoch) {
   if (!c) return nullptr;
+  // epoch > 0: that call's double-buffered slot; epoch <= 0: the fixed slot
+  // holding the most recently gathered matrix
+  const int64_t slot = epoch > 0 ? (epoch & 1) : 2;
   return reinterpret_cast<int64_t*>(c->base + c->demand_off) +
-         (epoch & 1) * ((int64_t)c->world * c->world + c->world);
+         slot * ((int64_t)c->world * c->world + c->world);
 }
 int64_t fast_comm_recv_capacity(const fast_comm* c) { return c ? c->recv_bytes : 0; }
 int64_t fast_comm_staging_capacity(const fast_comm* c) { return c ? c->staging_bytes : 0; }
@@ -762,7 +809,8 @@ int fast_exec(fast_comm* c, const fast_plan* plan, const void* send, int64_t epo
 static int exec_launch(fast_comm* c, const fast_plan* plan, const void* send, int64_t epoch,
                        int blocks, int64_t chunk_bytes, int64_t* timeline_ns, void* stream,
                        int skip_barrier) {
-  if (!c || !c->opened || !plan || epoch < 1 || blocks < 1 || chunk_bytes < 16)
+  // epoch 0: the kernel reads this call's epoch from the device counter
+  if (!c || !c->opened || !plan || epoch < 0 || blocks < 1 || chunk_bytes < 16)
     return FAST_EVALIDATION;
   if (blocks > max_resident_blocks()) return FAST_EVALIDATION;
   ExecArgs a;
@@ -871,8 +919,9 @@ static int launch_fused(fast_comm* c, const void* send, const int64_t* counts, i
     fused_resident = sms * per_sm;
   }
   if (blocks > fused_resident) return FAST_EVALIDATION;
-  const int64_t e = c->epoch + 1;
-  c->epoch = e;
+  // device-side epoch (graph-capturable): bump it, the kernel reads it
+  bump_epoch_kernel<<<1, 1, 0, stream>>>(c->base);
+  c->epoch += 1;
   ExecArgs a;
   memset(&a, 0, sizeof(a));
   a.peers = c->peers_dev;
@@ -883,7 +932,7 @@ static int launch_fused(fast_comm* c, const void* send, const int64_t* counts, i
   a.recv_off = c->recv_off;
   a.staging_off = c->staging_off;
   a.chunk = chunk_bytes & ~(int64_t)15;
-  a.epoch = e;
+  a.epoch = 0;
   a.timeline = timeline_ns;
   a.rank = c->rank;
   a.world = c->world;
@@ -927,23 +976,26 @@ int fast_alltoallv(fast_comm* c, const void* send, const int64_t* counts, int n,
   if (!c->no_fuse && n <= kFusedMaxN && fused_smem_bytes(n, m) <= 200 * 1024)
     return launch_fused(c, send, counts, n, m, sched, plan, blocks, chunk_bytes, timeline_ns,
                         (cudaStream_t)stream);
-  const int64_t e = c->epoch + 1;
-  int rc = fast_gather_demand(c, counts, e, stream);
-  if (rc != FAST_OK) return rc;
-  c->epoch = e;
-  int64_t* D = fast_comm_demand_ptr(c, e);
+  // device-side epoch (gather_demand_kernel bumps it): every argument below
+  // is call-invariant, so the whole call can be captured in a CUDA graph
+  gather_demand_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(c->peers_dev, counts, 0, c->rank,
+                                                           c->world, c->demand_off);
+  if (cudaGetLastError() != cudaSuccess) return FAST_ECUDA;
+  c->epoch += 1;
+  int rc;
+  int64_t* D = fast_comm_demand_ptr(c, 0);
   rc = fast_synth_batch(D, 1, n, m, sched, stream);
   if (rc != FAST_OK) return rc;
   rc = fast_plan_compile(D, D + (int64_t)c->world * c->world, n, m, sched, c->recv_bytes,
                          c->staging_bytes, chunk_bytes, plan, stream);
   if (rc != FAST_OK) return rc;
-  return exec_launch(c, plan, send, e, blocks, chunk_bytes, timeline_ns, stream, 1);
+  return exec_launch(c, plan, send, 0, blocks, chunk_bytes, timeline_ns, stream, 1);
 }
 
 int64_t fast_comm_epoch(const fast_comm* c) { return c ? c->epoch : -1; }
 
 int fast_comm_set_epoch(fast_comm* c, int64_t epoch) {
-  if (!c || epoch < c->epoch) return FAST_EVALIDATION;
+  if (!c || epoch < 0) return FAST_EVALIDATION;
   c->epoch = epoch;
   return FAST_OK;
 }

@@ -171,11 +171,15 @@ class FastComm:
         self.recv = bytes_view(lib.fast_comm_recv_ptr(ptr), self.recv_bytes, self.device)
         self._sched_ref = ctypes.byref(self.sched.struct)
         self._plan_ref = ctypes.byref(self.plan.struct)
+        self.use_graph = True
+        self._fused = False
+        self._graphs: dict = {}
 
     def set_fused(self, enable: bool) -> None:
         """Single-launch path (gather + synthesis + plan inside the exec
         kernel, n <= 6) on/off; off by default (not faster on B200)."""
         _lib.check_rc(_lib.load().fast_comm_set_fused(self._ptr, 1 if enable else 0), "set_fused")
+        self._fused = bool(enable)
 
     def close(self) -> None:
         if getattr(self, "_ptr", None):
@@ -191,13 +195,13 @@ class FastComm:
     def demand(self) -> torch.Tensor:
         """The gathered G x G demand matrix of the last call (device)."""
         lib = _lib.load()
-        ptr = lib.fast_comm_demand_ptr(self._ptr, self.epoch)
+        ptr = lib.fast_comm_demand_ptr(self._ptr, 0)  # fixed slot: latest gathered matrix
         G = self.world
         return bytes_view(ptr, G * G * 8, self.device).view(torch.int64).view(G, G)
 
     def self_sizes(self) -> torch.Tensor:
         lib = _lib.load()
-        ptr = lib.fast_comm_demand_ptr(self._ptr, self.epoch) + 8 * self.world * self.world
+        ptr = lib.fast_comm_demand_ptr(self._ptr, 0) + 8 * self.world * self.world
         return bytes_view(ptr, self.world * 8, self.device).view(torch.int64)
 
     def alltoallv(self, send: torch.Tensor, send_counts: torch.Tensor,
@@ -220,12 +224,21 @@ class FastComm:
         s = stream or torch.cuda.current_stream()
         tl = ctypes.c_void_p(self.timeline.data_ptr()) if record_timeline else None
         if exec_events is None:
+            key = (send.data_ptr(), row.data_ptr(), bool(record_timeline), self._fused)
+            g = self._graphs.get(key) if (self.use_graph and stream is None) else None
+            if g is not None:  # one graph launch per call
+                g.replay()
+                self.epoch += 1
+                return self.recv
+            lib.fast_comm_set_epoch(self._ptr, self.epoch)  # graph replays bypass the host mirror
             _lib.check_rc(lib.fast_alltoallv(self._ptr, ctypes.c_void_p(send.data_ptr()),
                                              ctypes.c_void_p(row.data_ptr()), n, m,
                                              self._sched_ref, self._plan_ref, self.blocks,
                                              self.chunk, tl, ctypes.c_void_p(s.cuda_stream)),
                           "fast_alltoallv")
             self.epoch += 1
+            if self.use_graph and stream is None and len(self._graphs) < 16:
+                self._capture(key, send, row, tl)
             return self.recv
         # step by step (exec-kernel events for the benchmark)
         self.epoch += 1
@@ -248,6 +261,22 @@ class FastComm:
         exec_events[1].record(s)
         _lib.check_rc(lib.fast_comm_set_epoch(self._ptr, self.epoch), "fast_comm_set_epoch")
         return self.recv
+
+    def _capture(self, key, send: torch.Tensor, row: torch.Tensor, tl) -> None:
+        """Capture fast_alltoallv for this (send, counts) pair into a CUDA
+        graph (capture only records; the call above did the work)."""
+        lib = _lib.load()
+        n, m = self.topology.n_servers, self.topology.gpus_per_server
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            cs = torch.cuda.current_stream()
+            rc = lib.fast_alltoallv(self._ptr, ctypes.c_void_p(send.data_ptr()),
+                                    ctypes.c_void_p(row.data_ptr()), n, m, self._sched_ref,
+                                    self._plan_ref, self.blocks, self.chunk, tl,
+                                    ctypes.c_void_p(cs.cuda_stream))
+        _lib.check_rc(rc, "fast_alltoallv (capture)")
+        lib.fast_comm_set_epoch(self._ptr, self.epoch)  # capture did not execute
+        self._graphs[key] = g
 
     def check(self) -> None:
         """Raise if the last call's device status reports a failure (syncs)."""

@@ -91,6 +91,72 @@ def test_device_plan_equals_host_plan():
     comm.close()
 
 
+def _device_plan(D, n, m, selfb, recv_cap, staging_cap, chunk):
+    """fast_synth_batch + fast_plan_compile (CTA-parallel build) on cuda:0."""
+    import ctypes
+
+    from paper_2505_09764_b200 import _lib, synth
+    from paper_2505_09764_b200.executor import PlanBuffers
+
+    lib = _lib.load()
+    Dd = torch.from_numpy(D).cuda().view(1, n * m, n * m)
+    sd = torch.from_numpy(selfb).cuda()
+    bufs = synth.SynthBuffers(1, n, m)
+    plan = PlanBuffers(n, m, "cuda")
+    sh = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert lib.fast_synth_batch(ctypes.c_void_p(Dd.data_ptr()), 1, n, m,
+                                ctypes.byref(bufs.struct), sh) == 0
+    assert lib.fast_plan_compile(ctypes.c_void_p(Dd.data_ptr()), ctypes.c_void_p(sd.data_ptr()),
+                                 n, m, ctypes.byref(bufs.struct), recv_cap, staging_cap, chunk,
+                                 ctypes.byref(plan.struct), sh) == 0
+    torch.cuda.synchronize()
+    return plan.host_ops(), plan.staging_used.cpu().numpy(), int(plan.status.item())
+
+
+@pytest.mark.parametrize("n,m", [(2, 1), (2, 2), (2, 4), (4, 2), (3, 3), (8, 1), (2, 8),
+                                 (4, 4), (5, 2), (6, 3), (3, 8)])
+def test_parallel_device_plan_equals_host_plan(n, m):
+    """The CTA-parallel device plan (plan_par.cuh) is op-for-op identical to
+    the sequential host build (plan.cuh) -- Zipf, sparse, uniform and
+    hotspot matrices, power-of-two and odd chunk sizes, with self segments."""
+    G = n * m
+    rng = np.random.default_rng(7 * G + m)
+    sparse = rng.integers(1, 900_000, (G, G)).astype(np.int64)
+    sparse[rng.random((G, G)) < 0.6] = 0
+    np.fill_diagonal(sparse, 0)
+    cases = [workloads.zipf_sizes(5, G, 1.2, 40_000_003), sparse,
+             workloads.gen_uniform(3, Topology(n, m), 65_537).sizes,
+             workloads.gen_hotspot(4, Topology(n, m), 3_000_001, G - 1, 8).sizes,
+             np.ones((G, G), np.int64) - np.eye(G, dtype=np.int64)]
+    for ci, D in enumerate(cases):
+        D = np.ascontiguousarray(D, dtype=np.int64)
+        selfb = rng.integers(0, 5000, G).astype(np.int64) if ci % 2 else np.zeros(G, np.int64)
+        out = oracle.synthesize_batch(D, n, m)
+        p = PackedSchedule(**oracle.packed_fields(out, 0, n, m))
+        cap = int((D.sum(axis=0) + selfb).max()) + 64
+        stg = 4 * cap + (1 << 20)
+        for chunk in (64 * 1024, 1 << 20, 48 * 1024 + 16):
+            host_ops, used, st = plan_compile_host(D, n, m, p.stage_order, p.stage_perm,
+                                                   p.stage_bytes, cap, stg, send_self=selfb,
+                                                   chunk=chunk)
+            dev_ops, dused, dst = _device_plan(D, n, m, selfb, cap, stg, chunk)
+            assert st == 0 and dst == 0, (ci, chunk, st, dst)
+            assert dev_ops.dtype == OP_DTYPE
+            assert np.array_equal(dev_ops, host_ops), (ci, chunk, len(dev_ops), len(host_ops))
+            assert np.array_equal(dused, used), (ci, chunk)
+    # too-small receive / staging buffers: same status as the host build
+    D = np.ascontiguousarray(cases[0], dtype=np.int64)
+    out = oracle.synthesize_batch(D, n, m)
+    p = PackedSchedule(**oracle.packed_fields(out, 0, n, m))
+    z = np.zeros(G, np.int64)
+    for rc, sc in [(16, 1 << 40), (1 << 40, 16)]:
+        _, _, st = plan_compile_host(D, n, m, p.stage_order, p.stage_perm, p.stage_bytes, rc, sc,
+                                     send_self=z, chunk=1 << 20)
+        _, _, dst = _device_plan(D, n, m, z, rc, sc, 1 << 20)
+        assert st == dst, (rc, sc, st, dst)
+        assert rc > 16 or st != 0
+
+
 def test_group_exec_reports_small_buffers():
     n, m = 2, 2
     D = workloads.zipf_sizes(1, 4, 0.5, 100_000)

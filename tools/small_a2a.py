@@ -13,8 +13,9 @@ send = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
 row = torch.from_numpy(D[rank].copy()).cuda()
 for _ in range(20): comm.alltoallv(send, row)
 torch.cuda.synchronize(); dist.barrier()
-for fused in (True, False):
+for fused, graph in ((True, False), (False, False), (False, True)):
     comm.set_fused(fused)
+    comm.use_graph = graph
     for _ in range(20): comm.alltoallv(send, row)
     torch.cuda.synchronize(); dist.barrier()
     t = time.perf_counter()
@@ -26,7 +27,7 @@ for fused in (True, False):
     for _ in range(200): comm.alltoallv(send, row)
     b.record(); torch.cuda.synchronize()
     comm.check()
-    if rank == 0: print(f"per call (fused={fused}): wall {host_us:.1f} us, events {a.elapsed_time(b)/200*1e3:.1f} us", flush=True)
+    if rank == 0: print(f"per call (fused={fused}, graph={graph}): wall {host_us:.1f} us, events {a.elapsed_time(b)/200*1e3:.1f} us", flush=True)
 comm.close(); dist.destroy_process_group()
 
 # ---- per-stage device breakdown (events between the enqueued stages) ----
