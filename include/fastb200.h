@@ -319,6 +319,67 @@ int fast_moe_combine(const void *comb_recv, const void *expert_out,
                      const void *workspace, int E, const int64_t *seg_rows,
                      const float *weights, void *out, void *stream);
 
+/* ------------------------------------------------------------------------
+ * Analytical cost model, batched.  Replaces the
+ * reference's per-schedule Python model:
+ *   simulate_fast        simulate.py:107-193  -> t_balance .. total
+ *   simulate_spreadout   simulate.py:196-242  -> so_* (server / demand mode)
+ *   spreadout_stages     spreadout.py:19-31   -> so_weight
+ *   optimal_time, fast_worstcase_time, intra_assumption_holds
+ *                        bounds.py:27-76      -> t_optimal, t_worstcase, assumption_ok
+ * Same operation order in IEEE double as the reference's Python floats, so
+ * every output is bit-identical (tests/test_simulate.py).  Status per
+ * matrix: FAST_OK, FAST_EVALIDATION (stages not ascending), FAST_EINVARIANT
+ * (stage bytes disagree with the tables, floor violated), or the synthesis
+ * status passed in.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  double scaleup_bw;   /* B1, bytes/s */
+  double scaleout_bw;  /* B2, bytes/s */
+  double wakeup_delay; /* alpha, s */
+} fast_sim_topo;
+
+typedef struct {
+  const int64_t *balanced;     /* [B][G][G] cross tiles = redistribution tables,
+                                  intra tiles = the original blocks */
+  const int64_t *server;       /* [B][n][n] tile totals, diagonal S_i */
+  const int64_t *common_sum;   /* [B] max_rc of server */
+  const int32_t *move_count;   /* [B][T] balance moves per cross tile */
+  const fast_move *moves;      /* [B][T][move_slots] */
+  const int32_t *n_stages;     /* [B] sorted stages */
+  const int32_t *stage_order;  /* [B][stage_stride] row of the k-th stage */
+  const int64_t *stage_weight; /* [B][stage_stride] by row */
+  const uint8_t *stage_perm;   /* [B][stage_stride][n] */
+  const int64_t *stage_bytes;  /* [B][stage_stride][n]; 0 = no edge,
+                                  -1 = an edge carrying 0 bytes */
+  const int32_t *status;       /* [B] synthesis status, or NULL */
+  const int64_t *demand;       /* [B][G][G] original demand for the spreadout
+                                  demand mode, or NULL */
+  int move_slots;
+  int stage_stride;
+} fast_sim_in;
+
+typedef struct {
+  double *t_balance;      /* [B] */
+  double *t_intra;        /* [B] */
+  double *scale_out;      /* [B][stage_stride] */
+  double *redistribution; /* [B][stage_stride] */
+  double *total;          /* [B] */
+  double *t_optimal;      /* [B] */
+  double *t_worstcase;    /* [B] */
+  int32_t *assumption_ok; /* [B] */
+  int64_t *so_weight;     /* [B][n-1] spreadout stage weights */
+  double *so_server;      /* [B][n-1] spreadout durations, server-level mode */
+  double *so_demand;      /* [B][n-1] demand mode (needs in->demand), or NULL */
+  double *so_total;       /* [B][2] server-level / demand-mode totals */
+  int32_t *status;        /* [B] */
+  void *workspace;        /* fast_sim_workspace_bytes(B, n, m, stage_stride) */
+} fast_sim_out;
+
+size_t fast_sim_workspace_bytes(int B, int n, int m, int stage_stride);
+int fast_simulate_batch(const fast_sim_in *in, int B, int n, int m,
+                        const fast_sim_topo *topo, fast_sim_out *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

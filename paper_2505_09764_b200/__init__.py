@@ -52,8 +52,17 @@ _LAZY = {
     "build_balance_plan": "synth", "decompose_server_matrix": "synth",
     "embed_doubly_stochastic": "synth", "decompose": "synth",
     # executor
-    "Timeline": "executor", "FastComm": "executor", "execute_fast": "executor",
-    "all_to_all_fast": "executor", "simulate_fast": "executor",
+    "FastComm": "executor", "execute_fast": "executor", "all_to_all_fast": "executor",
+    # analytical cost model + baseline + bounds (device kernel csrc/sim.cu)
+    "Timeline": "simulate", "simulate_fast": "simulate", "simulate_batch": "simulate",
+    "simulate_spreadout": "simulate", "SimBuffers": "simulate", "step_cost": "simulate",
+    "intra_phase_time": "simulate", "split_deliveries": "simulate",
+    "stage_redistribution": "simulate", "spreadout_stages": "simulate",
+    "spreadout_completion_units": "simulate", "spreadout_intra": "simulate",
+    "synthesize_spreadout": "simulate", "SpreadoutSchedule": "simulate",
+    "BoundsReport": "simulate", "bounds_report": "simulate", "optimal_time": "simulate",
+    "fast_worstcase_time": "simulate", "ratio_bound": "simulate",
+    "intra_assumption_holds": "simulate",
     # MoE front-end
     "MoEDispatch": "moe",
 }

@@ -12,6 +12,31 @@ I64 = ctypes.c_int64
 P_SCHED = ctypes.POINTER(FastSchedBufs)
 P_PLAN = ctypes.POINTER(FastPlan)
 
+
+class FastSimTopo(ctypes.Structure):
+    """fast_sim_topo (include/fastb200.h)."""
+
+    _fields_ = [("scaleup_bw", ctypes.c_double), ("scaleout_bw", ctypes.c_double),
+                ("wakeup_delay", ctypes.c_double)]
+
+
+class FastSimIn(ctypes.Structure):
+    """fast_sim_in: packed schedules to evaluate."""
+
+    _fields_ = [(name, ctypes.c_void_p) for name in (
+        "balanced", "server", "common_sum", "move_count", "moves", "n_stages", "stage_order",
+        "stage_weight", "stage_perm", "stage_bytes", "status", "demand")] + [
+        ("move_slots", ctypes.c_int), ("stage_stride", ctypes.c_int)]
+
+
+class FastSimOut(ctypes.Structure):
+    """fast_sim_out: per-schedule model outputs."""
+
+    _fields_ = [(name, ctypes.c_void_p) for name in (
+        "t_balance", "t_intra", "scale_out", "redistribution", "total", "t_optimal",
+        "t_worstcase", "assumption_ok", "so_weight", "so_server", "so_demand", "so_total",
+        "status", "workspace")]
+
 SIGNATURES: list[tuple[str, object, list]] = [
     # executor: plan compile (exec.cu / plan.cuh)
     ("fast_plan_workspace_bytes", ctypes.c_size_t, [I, I]),
@@ -39,6 +64,10 @@ SIGNATURES: list[tuple[str, object, list]] = [
     ("fast_debug_copy", I, [V, V, I64, I, I64, I, V]),
     ("fast_comm_create_group", I, [I, I64, I64, ctypes.POINTER(V)]),
     ("fast_exec_group", I, [ctypes.POINTER(V), I, P_PLAN, ctypes.POINTER(V), I64, I, I64, V, V]),
+    # analytical cost model (sim.cu)
+    ("fast_sim_workspace_bytes", ctypes.c_size_t, [I, I, I, I]),
+    ("fast_simulate_batch", I, [ctypes.POINTER(FastSimIn), I, I, I, ctypes.POINTER(FastSimTopo),
+                                ctypes.POINTER(FastSimOut), V]),
     # MoE front-end (moe.cu)
     ("fast_moe_gate", I, [I, ctypes.c_uint64, I, V, V, V, V]),
     ("fast_moe_route_workspace_bytes", ctypes.c_size_t, [I, I, I]),

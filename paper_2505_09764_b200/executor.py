@@ -27,6 +27,7 @@ import torch
 
 from . import _lib
 from .model import Topology, ValidationError, validate_topology
+from .simulate import Timeline
 from .synth import SynthBuffers, _device, _stream_handle
 
 OP_DTYPE = np.dtype([("src_off", "<i8"), ("dst_off", "<i8"), ("len", "<i8"),
@@ -38,25 +39,6 @@ BUF_SEND, BUF_RECV, BUF_STAGING = 0, 1, 2
 TIMELINE_STRIDE = 8 + 256
 DEFAULT_BLOCKS = 128  # one 512-thread CTA per SM; must stay <= SM count (co-residency)
 DEFAULT_CHUNK = 1024 * 1024
-
-
-@dataclass(frozen=True)
-class Timeline:
-    """Per-phase breakdown, shaped like tiersched's (simulate.py:38-55), but
-    MEASURED on the device (seconds).  scale_out[k] is the time from the
-    barrier until stage k's bytes had all arrived at this rank's staging
-    (0 where this rank proxies nothing in stage k)."""
-
-    t_balance: float
-    t_intra_a2a: float
-    scale_out: tuple[float, ...]
-    redistribution: tuple[float, ...]
-    total: float
-
-    def to_json_dict(self) -> dict:
-        return {"t_balance": self.t_balance, "t_intra_a2a": self.t_intra_a2a,
-                "scale_out": list(self.scale_out), "redistribution": list(self.redistribution),
-                "total": self.total}
 
 
 class _CudaBytes:
@@ -420,9 +402,3 @@ class GroupComm:
 def execute_fast(comm: FastComm, send: torch.Tensor, send_counts: torch.Tensor) -> torch.Tensor:
     """Alias of comm.alltoallv (the executor behind simulate_fast's API)."""
     return comm.alltoallv(send, send_counts)
-
-
-def simulate_fast(*args, **kwargs):  # pragma: no cover - API pointer
-    raise NotImplementedError(
-        "the analytical cost model is out of scope on B200; use FastComm.alltoallv + "
-        "measured_timeline() (the executor this path replaces)")
