@@ -104,6 +104,30 @@ int fast_balance_batch(const int64_t *D, int B, int n, int m,
 int fast_decompose_batch(const int64_t *S, int B, int n, int mode,
                          const fast_sched_bufs *out, void *stream);
 
+/* Stage-level building blocks of the Birkhoff module, standalone
+ * (csrc/stages.cu; the batched synthesis fuses them).
+ *
+ * find_perfect_matching (birkhoff.py:111-137) for B boolean supports
+ * [B][n][n] (non-zero = edge): rows in index order, columns scanned in
+ * index order, fresh `seen` per root.  row_match[b][u] = matched column,
+ * status[b] FAST_EINVARIANT (and row_match -1) when no perfect matching. */
+int fast_match_batch(const uint8_t *support, int B, int n, int32_t *row_match,
+                     int32_t *status, void *stream);
+
+/* strip_auxiliary (birkhoff.py:225-252, mode bit 1) and/or
+ * sort_stages_ascending (birkhoff.py:255-266, mode bit 2) on one stage
+ * list of K stages over n servers: weight[K], dst[K][n] (-1 = no edge from
+ * that source), bytes[K][n], aux[n][n] (strip only).  real_out[K][n]: the
+ * edges' bytes after stripping; order_out[0..n_out): input positions of the
+ * resulting stages in output order (kept stages in decomposition order, or
+ * sorted by (weight, first edge, position)).  status FAST_EINVARIANT when
+ * auxiliary bytes are left unconsumed. */
+size_t fast_strip_sort_workspace_bytes(int K, int n);
+int fast_strip_sort(const int64_t *weight, const int16_t *dst, const int64_t *bytes,
+                    const int64_t *aux, int K, int n, int mode, int32_t *order_out,
+                    int64_t *real_out, int32_t *n_out, int32_t *status, void *workspace,
+                    void *stream);
+
 /* ------------------------------------------------------------------------
  * Executor: P2P stage execution over NVSwitch (replaces the reference's
  * analytical "executor" simulate_fast, simulate.py:107-193, with real data

@@ -11,6 +11,8 @@ reached through the C-ABI in include/fastb200.h; there is no CPU fallback.
 
 from .model import (
     MAX_SAFE_TOTAL,
+    load_matrix,
+    save_matrix,
     DemandMatrix,
     InternalInvariantError,
     ServerMatrix,
@@ -33,7 +35,7 @@ from .schedule import (
     schedule_from_json,
     schedule_to_json,
 )
-from .workloads import gen_adversarial, gen_hotspot, gen_uniform, gen_zipf
+from .workloads import gen_adversarial, gen_hotspot, gen_uniform, gen_zipf, load_trace
 
 
 def algorithmic_bandwidth(total_bytes: int, gpu_count: int, completion_s: float) -> float:
@@ -51,6 +53,8 @@ _LAZY = {
     "synthesize_packed": "synth", "SynthBuffers": "synth",
     "build_balance_plan": "synth", "decompose_server_matrix": "synth",
     "embed_doubly_stochastic": "synth", "decompose": "synth",
+    "balance_senders": "synth", "merge_peer": "synth", "find_perfect_matching": "synth",
+    "strip_auxiliary": "synth", "sort_stages_ascending": "synth",
     # executor
     "FastComm": "executor", "execute_fast": "executor", "all_to_all_fast": "executor",
     # analytical cost model + baseline + bounds (device kernel csrc/sim.cu)
@@ -81,7 +85,8 @@ __all__ = [
     "BalancePlan", "Decomposition", "DemandMatrix", "InternalInvariantError", "IntraMove",
     "MAX_SAFE_TOTAL", "PackedSchedule", "PermutationStage", "Schedule", "ServerMatrix",
     "TileView", "Topology", "ValidationError", "algorithmic_bandwidth", "dumps_canonical",
-    "gen_adversarial", "gen_hotspot", "gen_uniform", "gen_zipf", "max_rc",
+    "gen_adversarial", "gen_hotspot", "gen_uniform", "gen_zipf", "load_matrix", "load_trace",
+    "max_rc", "save_matrix",
     "reduce_to_server_level", "schedule_from_json", "schedule_to_json", "tile",
     "validate_topology", *_LAZY,
 ]

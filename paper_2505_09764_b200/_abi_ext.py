@@ -64,6 +64,10 @@ SIGNATURES: list[tuple[str, object, list]] = [
     ("fast_debug_copy", I, [V, V, I64, I, I64, I, V]),
     ("fast_comm_create_group", I, [I, I64, I64, ctypes.POINTER(V)]),
     ("fast_exec_group", I, [ctypes.POINTER(V), I, P_PLAN, ctypes.POINTER(V), I64, I, I64, V, V]),
+    # stage-level building blocks (stages.cu)
+    ("fast_match_batch", I, [V, I, I, V, V, V]),
+    ("fast_strip_sort_workspace_bytes", ctypes.c_size_t, [I, I]),
+    ("fast_strip_sort", I, [V, V, V, V, I, I, I, V, V, V, V, V, V]),
     # analytical cost model (sim.cu)
     ("fast_sim_workspace_bytes", ctypes.c_size_t, [I, I, I, I]),
     ("fast_simulate_batch", I, [ctypes.POINTER(FastSimIn), I, I, I, ctypes.POINTER(FastSimTopo),

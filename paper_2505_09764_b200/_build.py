@@ -18,7 +18,7 @@ CSRC = os.path.join(PKG_DIR, "csrc")
 INCLUDE = os.path.join(REPO_DIR, "include")
 LIB_PATH = os.path.join(PKG_DIR, "libfastb200.so")
 
-SOURCES = ["synth.cu", "exec.cu", "moe.cu", "sim.cu"]
+SOURCES = ["synth.cu", "exec.cu", "moe.cu", "sim.cu", "stages.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -26,10 +26,12 @@ import numpy as np
 import torch
 
 from . import _lib
-from .model import (DemandMatrix, InternalInvariantError, ServerMatrix, Topology,
+from .model import (DemandMatrix, InternalInvariantError, ServerMatrix, TileView, Topology,
                     ValidationError)
-from .schedule import (MOVE_DTYPE, BalancePlan, Decomposition, PackedSchedule,
-                       PermutationStage, Schedule)
+from .schedule import (MOVE_DTYPE, BalancePlan, Decomposition, IntraMove, PackedSchedule,
+                       PermutationStage, Schedule, _fast_stage)
+
+FAST_MAX_SERVERS = 128  # include/fastb200.h
 
 
 def stage_cap(n: int) -> int:
@@ -291,3 +293,126 @@ def synthesize_host_batch(D_host: torch.Tensor, n: int, m: int, out: HostSchedul
     for st in streams:
         st.synchronize()
     return out
+
+
+# ---------------------------------------------------------------------------
+# Stage-level building blocks of the reference's balance / Birkhoff modules
+# as standalone calls (the batched synthesis fuses them).
+def balance_senders(tv: TileView) -> tuple[np.ndarray, list[IntraMove]]:
+    """Equalize one cross tile's row sums (balance.py:77-126): the balance
+    kernel on a two-server embedding of the tile."""
+    if tv.is_intra:
+        raise ValidationError("balance_senders expects a cross-server tile")
+    e = np.asarray(tv.entries, dtype=np.int64)
+    m = e.shape[0]
+    if e.ndim != 2 or e.shape != (m, m):
+        raise ValidationError("tile must be square")
+    D = np.zeros((2 * m, 2 * m), np.int64)
+    D[:m, m:] = e
+    dev = _device()
+    Dt = torch.from_numpy(D[None].copy()).to(dev)
+    bufs = SynthBuffers(1, 2, m, dev)
+    rc = _lib.load().fast_balance_batch(ctypes.c_void_p(Dt.data_ptr()), 1, 2, m,
+                                        ctypes.byref(bufs.struct), _stream_handle(None))
+    _lib.check_rc(rc, "fast_balance_batch")
+    _raise_status(int(bufs.status.cpu()[0]), "balance_senders")
+    bal = bufs.balanced[0, :m, m:].cpu().numpy().copy()
+    cnt = int(bufs.move_count[0, 0].item())
+    mv = bufs.moves[0, 0, :cnt].cpu().numpy().view(MOVE_DTYPE).reshape(-1)
+    moves = [IntraMove(server=tv.src_server, from_gpu=int(x["from_gpu"]), to_gpu=int(x["to_gpu"]),
+                       for_dst_server=tv.dst_server, bytes=int(x["bytes"])) for x in mv]
+    return bal, moves
+
+
+def merge_peer(balanced_tile: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """diag(row sums) plus the redistribution table (balance.py:129-136)."""
+    rows = np.asarray(balanced_tile).sum(axis=1)
+    if rows.size and int(rows.max() - rows.min()) > 1:
+        raise ValidationError("merge_peer expects row sums differing by <= 1")
+    return np.diag(rows).astype(np.int64), np.asarray(balanced_tile).astype(np.int64, copy=True)
+
+
+def find_perfect_matching(support: np.ndarray) -> dict[int, int]:
+    """Deterministic perfect matching (birkhoff.py:111-137): the
+    decomposition's warp DFS (fast_match_batch)."""
+    sp = np.asarray(support)
+    if sp.ndim != 2 or sp.shape[0] != sp.shape[1]:
+        raise ValidationError("support must be a square matrix")
+    n = sp.shape[0]
+    if n == 0:
+        return {}
+    if n > FAST_MAX_SERVERS:
+        raise ValidationError(f"support larger than {FAST_MAX_SERVERS} rows")
+    dev = _device()
+    st = torch.from_numpy((sp != 0).astype(np.uint8)[None].copy()).to(dev)
+    rm = torch.empty((1, n), dtype=torch.int32, device=dev)
+    status = torch.empty(1, dtype=torch.int32, device=dev)
+    rc = _lib.load().fast_match_batch(ctypes.c_void_p(st.data_ptr()), 1, n,
+                                      ctypes.c_void_p(rm.data_ptr()),
+                                      ctypes.c_void_p(status.data_ptr()), _stream_handle(None))
+    _lib.check_rc(rc, "fast_match_batch")
+    if int(status.item()) != _lib.FAST_OK:
+        raise InternalInvariantError("support matrix has no perfect matching")
+    r = rm[0].cpu().numpy()
+    return {u: int(r[u]) for u in range(n)}
+
+
+def _strip_sort(stages: Sequence[PermutationStage], aux: np.ndarray | None, mode: int):
+    stages = list(stages)
+    K = len(stages)
+    n = 1
+    for st in stages:
+        for s, d, _ in st.edges:
+            n = max(n, int(s) + 1, int(d) + 1)
+    if aux is not None:
+        aux = np.asarray(aux, dtype=np.int64)
+        n = max(n, aux.shape[0])
+    Kc = max(K, 1)
+    w = np.zeros(Kc, np.int64)
+    dst = np.full((Kc, n), -1, np.int16)
+    b = np.zeros((Kc, n), np.int64)
+    for k, st in enumerate(stages):
+        w[k] = st.weight
+        for s, d, x in st.edges:
+            dst[k, s], b[k, s] = d, x
+    A = np.zeros((n, n), np.int64)
+    if aux is not None:
+        A[: aux.shape[0], : aux.shape[1]] = aux
+    dev = _device()
+    tt = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    wt, dt, bt, at = tt(w), tt(dst), tt(b), tt(A)
+    order = torch.empty(Kc, dtype=torch.int32, device=dev)
+    real = torch.empty((Kc, n), dtype=torch.int64, device=dev)
+    n_out = torch.zeros(1, dtype=torch.int32, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    lib = _lib.load()
+    ws = torch.empty(int(lib.fast_strip_sort_workspace_bytes(K, n)), dtype=torch.uint8,
+                     device=dev)
+    P = lambda x: ctypes.c_void_p(x.data_ptr())  # noqa: E731
+    rc = lib.fast_strip_sort(P(wt), P(dt), P(bt), P(at), K, n, mode, P(order), P(real), P(n_out),
+                             P(status), P(ws), _stream_handle(None))
+    _lib.check_rc(rc, "fast_strip_sort")
+    st = int(status.item())
+    if st != _lib.FAST_OK:
+        raise InternalInvariantError("auxiliary bytes left unconsumed")
+    k_out = int(n_out.item())
+    return stages, order[:k_out].cpu().numpy(), real.cpu().numpy(), dst
+
+
+def strip_auxiliary(stages: Sequence[PermutationStage], aux: np.ndarray) -> list[PermutationStage]:
+    """Charge the auxiliary padding greedily, drop emptied edges and stages
+    (birkhoff.py:225-252), on the device (fast_strip_sort)."""
+    stages, order, real, dst = _strip_sort(stages, aux, 1)
+    out = []
+    for k in order:
+        edges = tuple((u, int(dst[k, u]), int(real[k, u])) for u in range(dst.shape[1])
+                      if dst[k, u] >= 0 and real[k, u] > 0)
+        out.append(_fast_stage(stages[k].weight, edges))
+    return out
+
+
+def sort_stages_ascending(stages: Sequence[PermutationStage]) -> list[PermutationStage]:
+    """Stable sort by (weight, first (src, dst) edge) (birkhoff.py:255-266),
+    on the device (fast_strip_sort)."""
+    stages, order, _, _ = _strip_sort(stages, None, 2)
+    return [stages[int(k)] for k in order]

@@ -155,3 +155,10 @@ def gen_hotspot(seed: int, t: Topology, mean_bytes: int, hot: int, factor: int) 
     d[:, hot] *= factor
     np.fill_diagonal(d, 0)
     return DemandMatrix(t.n_servers, t.gpus_per_server, d)
+
+
+def load_trace(path: str) -> DemandMatrix:
+    """Load a demand matrix from a JSON or CSV trace file (workloads.py:88-90)."""
+    from .model import load_matrix
+
+    return load_matrix(path)
