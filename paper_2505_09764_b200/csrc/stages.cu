@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(kMatchWarps * 32)
     s.cm[v] = -1;
     s.newcol[v] = -1;
   }
+  for (int c = lane; c < n * NWP; c += 32) s.supc[c] = 0u;  // free columns: empty row
   __syncwarp();
   int st = FAST_OK;
   for (int u = 0; u < n; ++u) {  // rows in index order, fresh `seen` per root

@@ -36,7 +36,10 @@ namespace {
 #define FAST_BAL_STRIP_KB 16
 #endif
 constexpr int kBalThreads = FAST_BAL_THREADS;
-constexpr int kDecWarps = 4;  // matrices per CTA in decompose_kernel
+#ifndef FAST_DEC_WARPS
+#define FAST_DEC_WARPS 1
+#endif
+constexpr int kDecWarps = FAST_DEC_WARPS;  // matrices per CTA in decompose_kernel
 
 // Optional section timers (debug builds with -DFAST_DEC_PROFILE only).
 #ifdef FAST_DEC_PROFILE

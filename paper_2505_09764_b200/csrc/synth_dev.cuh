@@ -153,6 +153,7 @@ template <int NW>
 struct DecSh {
   static constexpr int NQ = (NW + 1) / 2;   // u64 words per support row
   static constexpr int NWP = 2 * NQ;        // u32 words per support row
+  static constexpr int kRowShift = NWP == 4 ? 4 : 3;  // log2 bytes per row
   uint32_t* sup;   // [n][NWP]
   uint32_t* supc;  // [n][NWP]
   int64_t* R;      // [n+1]
@@ -223,55 +224,188 @@ __device__ __forceinline__ void load_row64(const uint32_t* src, uint64_t& r0, ui
 }
 
 // Kuhn augment(root) with a fresh `seen` (birkhoff.py:172-180), one thread.
-// When a frame resumes after a failed child every support column left of
-// the failed one is already seen, so "first column of support & ~seen" is
-// exactly the reference's next v and no resume cursor is needed.  Returns
-// the depth of the successful path (pick[k] = column taken at depth k,
-// pick[depth] free) or -1.
-__device__ __forceinline__ int clz64(uint64_t x) {  // 64 for x == 0
-  const uint32_t hi = (uint32_t)(x >> 32), lo = (uint32_t)x;
-  return hi ? __clz(hi) : 32 + __clz(lo);
-}
+//
+// The search is a dependent chain (next row = supc[first(row & ~seen)]), so
+// the loop is written as one PTX block that keeps every step branch-free and
+// short: per-word clz -> candidate row addresses -> a two-level selp tree ->
+// ld.shared; `seen` is updated from the per-word clz (off the address chain).
+// When a frame resumes after a failed child every support column left of the
+// failed one is already seen, so "first column of support & ~seen" is exactly
+// the reference's next v and no resume cursor is needed.
+//
+// Free columns are recognised without a per-step test: supc[v] is all-zero
+// for a free column v, so stepping onto one ends in the (rare) "no unseen
+// column" exit, which tells the two cases apart with the freeb bitmap.
+// pick[k] holds the BYTE OFFSET of the k-th column's supc row (column =
+// pick >> kRowShift).  Returns the depth of the successful path (pick[depth]
+// is the free column) or -1.
+#define FAST_DFS_STEP4(R0, R1, R2, R3, N0, N1, N2, N3)                 \
+  "and.b32 x0, " R1 ", ns0;\n\t"                                      \
+  "and.b32 x1, " R0 ", ns1;\n\t"                                      \
+  "and.b32 x2, " R3 ", ns2;\n\t"                                      \
+  "and.b32 x3, " R2 ", ns3;\n\t"                                      \
+  "bfind.shiftamt.u32 z0, x0;\n\t"                                               \
+  "bfind.shiftamt.u32 z1, x1;\n\t"                                               \
+  "bfind.shiftamt.u32 z2, x2;\n\t"                                               \
+  "bfind.shiftamt.u32 z3, x3;\n\t"                                               \
+  "or.b32 t, x0, x1;\n\t"                                             \
+  "or.b32 u, x2, x3;\n\t"                                             \
+  "or.b32 u, u, t;\n\t"                                               \
+  "setp.eq.u32 pn, u, 0;\n\t"                                         \
+  "setp.ne.u32 p0, x0, 0;\n\t"                                        \
+  "setp.ne.u32 p2, x2, 0;\n\t"                                        \
+  "setp.ne.u32 p01, t, 0;\n\t"                                        \
+  "mad.lo.u32 a0, z0, 16, bb0;\n\t"                                   \
+  "mad.lo.u32 a1, z1, 16, bb1;\n\t"                                   \
+  "mad.lo.u32 a2, z2, 16, bb2;\n\t"                                   \
+  "mad.lo.u32 a3, z3, 16, bb3;\n\t"                                   \
+  "selp.b32 a0, a0, a1, p0;\n\t"                                      \
+  "selp.b32 a2, a2, a3, p2;\n\t"                                      \
+  "selp.b32 ad, a0, a2, p01;\n\t"                                     \
+  "ld.shared.v4.u32 {" N0 ", " N1 ", " N2 ", " N3 "}, [ad];\n\t"     \
+  "@pn bra.uni FDFS_BACK;\n\t"                                        \
+  "shr.u32 z0, hb, z0;\n\t"                                           \
+  "shr.u32 z1, hb, z1;\n\t"                                           \
+  "shr.u32 z2, hb, z2;\n\t"                                           \
+  "shr.u32 z3, hb, z3;\n\t"                                           \
+  "selp.b32 z3, 0, z3, p2;\n\t"                                       \
+  "not.b32 z0, z0;\n\t"                                               \
+  "not.b32 z1, z1;\n\t"                                               \
+  "not.b32 z2, z2;\n\t"                                               \
+  "not.b32 z3, z3;\n\t"                                               \
+  "and.b32 ns0, ns0, z0;\n\t"                                         \
+  "@!p0 and.b32 ns1, ns1, z1;\n\t"                                    \
+  "@!p01 and.b32 ns2, ns2, z2;\n\t"                                   \
+  "@!p01 and.b32 ns3, ns3, z3;\n\t"                                   \
+  "sub.u32 t, ad, bb0;\n\t"                                           \
+  "st.shared.u16 [pa], t;\n\t"                                        \
+  "add.u32 pa, pa, 2;\n\t"
+
+#define FAST_DFS_STEP2(R0, R1, N0, N1)                                 \
+  "and.b32 x0, " R1 ", ns0;\n\t"                                      \
+  "and.b32 x1, " R0 ", ns1;\n\t"                                      \
+  "bfind.shiftamt.u32 z0, x0;\n\t"                                               \
+  "bfind.shiftamt.u32 z1, x1;\n\t"                                               \
+  "or.b32 t, x0, x1;\n\t"                                             \
+  "setp.eq.u32 pn, t, 0;\n\t"                                         \
+  "setp.ne.u32 p0, x0, 0;\n\t"                                        \
+  "mad.lo.u32 a0, z0, 8, bb0;\n\t"                                    \
+  "mad.lo.u32 a1, z1, 8, bb1;\n\t"                                    \
+  "selp.b32 ad, a0, a1, p0;\n\t"                                      \
+  "ld.shared.v2.u32 {" N0 ", " N1 "}, [ad];\n\t"                     \
+  "@pn bra.uni FDFS_BACK;\n\t"                                        \
+  "shr.u32 z0, hb, z0;\n\t"                                           \
+  "shr.u32 z1, hb, z1;\n\t"                                           \
+  "not.b32 z0, z0;\n\t"                                               \
+  "not.b32 z1, z1;\n\t"                                               \
+  "and.b32 ns0, ns0, z0;\n\t"                                         \
+  "@!p0 and.b32 ns1, ns1, z1;\n\t"                                    \
+  "sub.u32 t, ad, bb0;\n\t"                                           \
+  "st.shared.u16 [pa], t;\n\t"                                        \
+  "add.u32 pa, pa, 2;\n\t"
+
+// Shared tail of both widths: the rare exits.  On "no unseen column" the
+// last pushed column is either free (success at depth sp-1) or a dead end
+// (pop it and resume its parent row); at sp == 0 the root is exhausted.
+#define FAST_DFS_BACK(SH, LDROW)                                        \
+  "FDFS_BACK:\n\t"                                                      \
+  "setp.eq.u32 pz, pa, %2;\n\t"                                         \
+  "@pz bra.uni FDFS_FAIL;\n\t"                                          \
+  "ld.shared.u16 t, [pa+-2];\n\t"                                       \
+  "shr.u32 t, t, " SH ";\n\t"                                           \
+  "shr.u32 u, t, 5;\n\t"                                                \
+  "xor.b32 u, u, 1;\n\t"                                                \
+  "mad.lo.u32 u, u, 4, %3;\n\t"                                         \
+  "ld.shared.u32 u, [u];\n\t"                                           \
+  "and.b32 t, t, 31;\n\t"                                               \
+  "shr.u32 t, hb, t;\n\t"                                               \
+  "and.b32 u, u, t;\n\t"                                                \
+  "setp.ne.u32 pz, u, 0;\n\t"                                           \
+  "@pz bra.uni FDFS_FOUND;\n\t"                                         \
+  "sub.u32 pa, pa, 2;\n\t"                                              \
+  "setp.eq.u32 pz, pa, %2;\n\t"                                         \
+  "mov.b32 ad, %1;\n\t"                                                 \
+  "@pz bra.uni FDFS_RELOAD;\n\t"                                        \
+  "ld.shared.u16 t, [pa+-2];\n\t"                                       \
+  "add.u32 ad, t, bb0;\n\t"                                             \
+  "FDFS_RELOAD:\n\t"                                                    \
+  LDROW                                                                 \
+  "bra.uni FDFS_LOOP;\n\t"                                              \
+  "FDFS_FOUND:\n\t"                                                     \
+  "sub.u32 t, pa, %2;\n\t"                                              \
+  "shr.u32 t, t, 1;\n\t"                                                \
+  "sub.u32 %0, t, 1;\n\t"                                               \
+  "bra.uni FDFS_END;\n\t"                                               \
+  "FDFS_FAIL:\n\t"                                                      \
+  "mov.b32 %0, -1;\n\t"                                                 \
+  "FDFS_END:\n\t"
 
 template <int NW>
-__device__ int dfs_search(const DecSh<NW>& s, const int root, uint64_t free0,
-                          uint64_t free1) {
+__device__ __noinline__ int dfs_search(const DecSh<NW>& s, const int root) {
   constexpr int NWP = DecSh<NW>::NWP;
-  uint64_t seen0 = 0ull, seen1 = 0ull, r0, r1;
-  load_row64<NW>(s.sup + root * NWP, r0, r1);
-  int sp = 0;
-  for (;;) {
-    const int z0 = clz64(r0 & ~seen0), z1 = clz64(r1 & ~seen1);
-    const int v = z0 < 64 ? z0 : 64 + z1;  // 128: no unseen support column
-    uint64_t n0, n1;
-    load_row64<NW>(s.supc + (v & 127) * NWP, n0, n1);  // speculative next row
-    if (__builtin_expect(v == 128, 0)) {
-      if (sp == 0) return -1;
-      --sp;
-      load_row64<NW>(sp == 0 ? s.sup + root * NWP : s.supc + s.pick[sp - 1] * NWP, r0, r1);
-      continue;
-    }
-    const uint64_t m = 0x8000000000000000ull >> (v & 63);
-    const bool hi = v >= 64;
-    const uint64_t fm = (hi ? free1 : free0) & m;
-    seen0 |= hi ? 0ull : m;
-    seen1 |= hi ? m : 0ull;
-    s.pick[sp] = (int16_t)v;
-    if (fm) return sp;
-    ++sp;
-    r0 = n0;
-    r1 = n1;
+  const uint32_t root_a = (uint32_t)__cvta_generic_to_shared(s.sup + root * NWP);
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(s.supc);
+  const uint32_t pick = (uint32_t)__cvta_generic_to_shared(s.pick);
+  const uint32_t freeb = (uint32_t)__cvta_generic_to_shared(s.freeb);
+  int depth;
+  if constexpr (NWP == 4) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p0, p2, p01, pn, pz;\n\t"
+        ".reg .b32 r0, r1, r2, r3, n0, n1, n2, n3, ns0, ns1, ns2, ns3;\n\t"
+        ".reg .b32 x0, x1, x2, x3, z0, z1, z2, z3, a0, a1, a2, a3;\n\t"
+        ".reg .b32 ad, t, u, pa, hb, bb0, bb1, bb2, bb3;\n\t"
+        "mov.b32 ns0, -1;\n\t"
+        "mov.b32 ns1, -1;\n\t"
+        "mov.b32 ns2, -1;\n\t"
+        "mov.b32 ns3, -1;\n\t"
+        "mov.b32 hb, 0x80000000;\n\t"
+        "mov.b32 pa, %2;\n\t"
+        "mov.b32 bb0, %4;\n\t"
+        "add.u32 bb1, %4, 512;\n\t"
+        "add.u32 bb2, %4, 1024;\n\t"
+        "add.u32 bb3, %4, 1536;\n\t"
+        "ld.shared.v4.u32 {r0, r1, r2, r3}, [%1];\n\t"
+        "FDFS_LOOP:\n\t"
+        FAST_DFS_STEP4("r0", "r1", "r2", "r3", "n0", "n1", "n2", "n3")
+        FAST_DFS_STEP4("n0", "n1", "n2", "n3", "r0", "r1", "r2", "r3")
+        "bra.uni FDFS_LOOP;\n\t"
+        FAST_DFS_BACK("4", "ld.shared.v4.u32 {r0, r1, r2, r3}, [ad];\n\t")
+        "}"
+        : "=r"(depth)
+        : "r"(root_a), "r"(pick), "r"(freeb), "r"(base)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p0, pn, pz;\n\t"
+        ".reg .b32 r0, r1, n0, n1, ns0, ns1, x0, x1, z0, z1, a0, a1;\n\t"
+        ".reg .b32 ad, t, u, pa, hb, bb0, bb1;\n\t"
+        "mov.b32 ns0, -1;\n\t"
+        "mov.b32 ns1, -1;\n\t"
+        "mov.b32 hb, 0x80000000;\n\t"
+        "mov.b32 pa, %2;\n\t"
+        "mov.b32 bb0, %4;\n\t"
+        "add.u32 bb1, %4, 256;\n\t"
+        "ld.shared.v2.u32 {r0, r1}, [%1];\n\t"
+        "FDFS_LOOP:\n\t"
+        FAST_DFS_STEP2("r0", "r1", "n0", "n1")
+        FAST_DFS_STEP2("n0", "n1", "r0", "r1")
+        "bra.uni FDFS_LOOP;\n\t"
+        FAST_DFS_BACK("3", "ld.shared.v2.u32 {r0, r1}, [ad];\n\t")
+        "}"
+        : "=r"(depth)
+        : "r"(root_a), "r"(pick), "r"(freeb), "r"(base)
+        : "memory");
   }
+  return depth;
 }
 
 // Lane 0 searches, the result is broadcast (the other lanes wait).
 template <int NW>
 __device__ __forceinline__ int dfs_warp(const DecSh<NW>& s, const int root) {
   int depth = 0;
-  if ((threadIdx.x & 31) == 0) {
-    const uint64_t* fq = reinterpret_cast<const uint64_t*>(s.freeb);
-    depth = dfs_search<NW>(s, root, fq[0], DecSh<NW>::NQ == 2 ? fq[1] : 0ull);
-  }
+  if ((threadIdx.x & 31) == 0) depth = dfs_search<NW>(s, root);
   return __shfl_sync(0xffffffffu, depth, 0);
 }
 
@@ -286,14 +420,14 @@ __device__ __forceinline__ void apply_path(const DecSh<NW>& s, const int root,
 #pragma unroll
   for (int j = 0; j < (FAST_MAX_SERVERS + 31) / 32; ++j) {
     const int k = j * 32 + lane;
-    rows[j] = (k <= depth) ? (k == 0 ? root : s.cm[s.pick[k - 1]]) : -1;
+    rows[j] = (k <= depth) ? (k == 0 ? root : s.cm[s.pick[k - 1] >> DecSh<NW>::kRowShift]) : -1;
   }
   __syncwarp();
 #pragma unroll
   for (int j = 0; j < (FAST_MAX_SERVERS + 31) / 32; ++j) {
     const int k = j * 32 + lane;
     if (k <= depth) {
-      const int v = s.pick[k], r = rows[j];
+      const int v = s.pick[k] >> DecSh<NW>::kRowShift, r = rows[j];
       s.cm[v] = (int16_t)r;
       s.newcol[r] = (int16_t)v;
 #pragma unroll
@@ -399,6 +533,7 @@ __device__ void decompose_one(char* wsm, const int64_t* __restrict__ S_all, cons
     for (int v = 0; v < n; ++v) s.C[v + 1] += s.C[v];
   }
   for (int u = lane; u < n; u += 32) s.cm[u] = -1;
+  for (int c = lane; c < n * NWP; c += 32) s.supc[c] = 0u;  // free columns: empty row
   if (lane < NWP) {
     s.chg[lane] = 0u;
     s.freeb[lane] = 0u;
@@ -538,6 +673,8 @@ __device__ void decompose_one(char* wsm, const int64_t* __restrict__ S_all, cons
       if (fr) {
         s.freed[nfreed + __popc(fb & ((1u << lane) - 1u))] = (int16_t)u;
         s.cm[rcol[r]] = -1;  // unmatch (birkhoff.py:210-214)
+#pragma unroll
+        for (int w = 0; w < NWP; ++w) s.supc[rcol[r] * NWP + w] = 0u;  // free: empty row
         atomicOr(&s.freeb[colword(rcol[r])], colbit(rcol[r]));
         rcol[r] = -1;
       }
