@@ -47,7 +47,6 @@ __global__ void __launch_bounds__(kMatchWarps * 32)
     for (int t = 0; t < 32; ++t)
       if (cb + t < n) bits |= 0x80000000u >> t;
     s.freeb[w] = bits;  // every column starts free
-    s.chg[w] = 0u;
   }
   for (int v = lane; v < n; v += 32) {
     s.cm[v] = -1;

@@ -110,6 +110,14 @@ __device__ __forceinline__ int64_t warp_min_i64(int64_t v) {
   }
   return v;
 }
+// min of non-negative int64 over the warp with two 32-bit redux.sync ops
+// (high words, then the low words of the lanes holding the minimal high word)
+__device__ __forceinline__ int64_t warp_min_nonneg_i64(int64_t v) {
+  const uint32_t hi = (uint32_t)((uint64_t)v >> 32), lo = (uint32_t)v;
+  const uint32_t mh = __reduce_min_sync(0xffffffffu, hi);
+  const uint32_t ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+  return (int64_t)(((uint64_t)mh << 32) | ml);
+}
 __device__ __forceinline__ int64_t warp_max_i64(int64_t v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -166,8 +174,8 @@ struct DecSh {
   int16_t* newcol; // [n]
   int16_t* pick;   // [n]
   int16_t* freed;  // [n]
-  uint32_t* chg;   // [NWP] rows whose match changed (bit r%32 of word r/32)
   uint32_t* freeb; // [NWP] free columns (cm < 0), support-bitset layout
+  int64_t* nvs;    // [n] value of a rematched row's new cell (cp.async'd in apply_path)
 };
 
 template <int NW>
@@ -178,8 +186,8 @@ __host__ __device__ __forceinline__ size_t dec_smem_bytes_t(int n) {
   b += (size_t)(2 * n + 2) * 8;            // auxl
   b += 3 * (size_t)n * 2 + 16;             // alo ahi aoff
   b += 4 * (size_t)n * 2;                  // cm newcol pick freed
-  b += NWP * 4 + 16;                       // chg
   b += NWP * 4 + 16;                       // freeb
+  b += (size_t)n * 8;                      // nvs
   return (b + 15) & ~(size_t)15;
 }
 
@@ -192,7 +200,7 @@ __device__ __forceinline__ DecSh<NW> dec_carve_t(char* p, int n) {
   s.R = (int64_t*)p; p += (size_t)(n + 1) * 8;
   s.C = (int64_t*)p; p += (size_t)(n + 1) * 8;
   s.auxl = (int64_t*)p; p += (size_t)(2 * n + 2) * 8;
-  s.chg = (uint32_t*)p; p += NWP * 4 + 16;
+  s.nvs = (int64_t*)p; p += (size_t)n * 8;
   s.freeb = (uint32_t*)p; p += NWP * 4 + 16;
   s.cm = (int16_t*)p; p += n * 2;
   s.newcol = (int16_t*)p; p += n * 2;
@@ -413,36 +421,46 @@ __device__ __forceinline__ int dfs_warp(const DecSh<NW>& s, const int root) {
 // root and row_{k+1} = old cm[pick[k]]; record new columns, refresh supc.
 template <int NW>
 __device__ __forceinline__ void apply_path(const DecSh<NW>& s, const int root,
-                                           const int depth, const int lane) {
+                                           const int depth, const int lane,
+                                           const int64_t* work = nullptr, const int n = 0) {
   constexpr int NWP = DecSh<NW>::NWP;
+  constexpr int J = (FAST_MAX_SERVERS + 31) / 32;
+  // an earlier path of this peel may still be filling nvs[] (same slots)
+  if (work) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncwarp();  // lane 0's pick[] writes visible to the warp
-  int rows[(FAST_MAX_SERVERS + 31) / 32];
+  const int jn = (depth >> 5) + 1;  // warp-uniform number of 32-element rounds
+  int rows[J], cols[J];
 #pragma unroll
-  for (int j = 0; j < (FAST_MAX_SERVERS + 31) / 32; ++j) {
+  for (int j = 0; j < J; ++j) {
     const int k = j * 32 + lane;
-    rows[j] = (k <= depth) ? (k == 0 ? root : s.cm[s.pick[k - 1] >> DecSh<NW>::kRowShift]) : -1;
+    rows[j] = -1;
+    cols[j] = 0;
+    if (j < jn && k <= depth) {
+      cols[j] = s.pick[k] >> DecSh<NW>::kRowShift;
+      rows[j] = k == 0 ? root : s.cm[s.pick[k - 1] >> DecSh<NW>::kRowShift];
+    }
   }
   __syncwarp();
 #pragma unroll
-  for (int j = 0; j < (FAST_MAX_SERVERS + 31) / 32; ++j) {
+  for (int j = 0; j < J; ++j) {
     const int k = j * 32 + lane;
-    if (k <= depth) {
-      const int v = s.pick[k] >> DecSh<NW>::kRowShift, r = rows[j];
+    if (j < jn && k <= depth) {
+      const int v = cols[j], r = rows[j];
+      // the row's new matched cell is read after the re-augmentation (peel
+      // loop, "rows whose cell changed"): copy it into smem asynchronously
+      if (work)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(s.nvs + r)),
+                     "l"(work + (int64_t)r * n + v)
+                     : "memory");
       s.cm[v] = (int16_t)r;
       s.newcol[r] = (int16_t)v;
 #pragma unroll
       for (int w = 0; w < NWP; ++w) s.supc[v * NWP + w] = s.sup[r * NWP + w];
-      atomicOr(&s.chg[r >> 5], 1u << (r & 31));
       if (k == depth) atomicAnd(&s.freeb[colword(v)], ~colbit(v));  // matched now
     }
   }
   __syncwarp();
-}
-
-// aux_left of cell (u, v): a slot of the row's staircase range, or -1.
-template <int NW>
-__device__ __forceinline__ int aux_slot(const DecSh<NW>& s, int u, int v) {
-  return (v >= s.alo[u] && v <= s.ahi[u]) ? s.aoff[u] + v - s.alo[u] : -1;
 }
 
 // The whole decomposition of matrix b by one warp; `wsm` is this warp's
@@ -534,10 +552,7 @@ __device__ void decompose_one(char* wsm, const int64_t* __restrict__ S_all, cons
   }
   for (int u = lane; u < n; u += 32) s.cm[u] = -1;
   for (int c = lane; c < n * NWP; c += 32) s.supc[c] = 0u;  // free columns: empty row
-  if (lane < NWP) {
-    s.chg[lane] = 0u;
-    s.freeb[lane] = 0u;
-  }
+  if (lane < NWP) s.freeb[lane] = 0u;
   __syncwarp();
   for (int v = lane; v < n; v += 32) atomicOr(&s.freeb[colword(v)], colbit(v));
   __syncwarp();
@@ -608,8 +623,10 @@ __device__ void decompose_one(char* wsm, const int64_t* __restrict__ S_all, cons
     if (lane == 0) { *status = st; out.n_raw[b] = 0; out.n_stages[b] = 0; }
     return;
   }
-  // lane-owned row state
-  int rcol[NW];
+  // lane-owned row state; the row's staircase range (alo, ahi, aoff) is
+  // constant, so aux slots are register arithmetic: slot = v - base if
+  // alo <= v <= ahi
+  int rcol[NW], alo[NW], ahi[NW], abase[NW];
   int64_t mv[NW], am[NW];
 #pragma unroll
   for (int r = 0; r < NW; ++r) {
@@ -617,15 +634,19 @@ __device__ void decompose_one(char* wsm, const int64_t* __restrict__ S_all, cons
     rcol[r] = -1;
     mv[r] = INT64_MAX;
     am[r] = 0;
+    alo[r] = 0;
+    ahi[r] = -1;
+    abase[r] = 0;
     if (u < n) {
       const int v = s.newcol[u];
       rcol[r] = v;
       mv[r] = work[(int64_t)u * n + v];
-      const int sl = aux_slot<NW>(s, u, v);
-      am[r] = sl >= 0 ? s.auxl[sl] : 0;
+      alo[r] = s.alo[u];
+      ahi[r] = s.ahi[u];
+      abase[r] = s.aoff[u] - alo[r];
+      am[r] = (v >= alo[r] && v <= ahi[r]) ? s.auxl[abase[r] + v] : 0;
     }
   }
-  if (lane < NWP) s.chg[lane] = 0u;
   __syncwarp();
 
   // ---- peel loop (birkhoff.py:190-219) fused with strip -----------------
@@ -640,7 +661,7 @@ __device__ void decompose_one(char* wsm, const int64_t* __restrict__ S_all, cons
     int64_t wl = INT64_MAX;
 #pragma unroll
     for (int r = 0; r < NW; ++r) wl = mv[r] < wl ? mv[r] : wl;
-    const int64_t weight = warp_min_i64(wl);
+    const int64_t weight = warp_min_nonneg_i64(wl);  // matched cells are > 0
     if (weight <= 0) { st = FAST_EINVARIANT; break; }
     remaining -= weight;
     int src0 = -1, nfreed = 0, dst0 = 0;
@@ -701,7 +722,7 @@ __device__ void decompose_one(char* wsm, const int64_t* __restrict__ S_all, cons
       const int depth = dfs_warp<NW>(s, u);
       DPROF_T(tb);
       if (depth < 0) { st = FAST_EINVARIANT; break; }
-      apply_path<NW>(s, u, depth, lane);
+      apply_path<NW>(s, u, depth, lane, work, n);
       DPROF_T(tc);
       DPROF_ADD(1, tb - ta);
       DPROF_ADD(2, tc - tb);
@@ -709,35 +730,39 @@ __device__ void decompose_one(char* wsm, const int64_t* __restrict__ S_all, cons
     }
     if (st != FAST_OK) break;
     DPROF_T(t2);
-    // rows whose cell changed: write the old (non-zero) value back, fetch
-    // the new cell; all loads are issued before any is consumed.
-    uint32_t chg[NW];
-#pragma unroll
-    for (int w = 0; w < NW; ++w) chg[w] = s.chg[w];
+    // rows whose cell changed (newcol != rcol): fetch the new cell's value
+    // (nvs, copied by apply_path) and aux_left, then write the old cell's
+    // value and aux_left back.  Loads first, stores after: slots of distinct
+    // cells never alias.
+    asm volatile("cp.async.wait_all;" ::: "memory");  // nvs[] from apply_path
     __syncwarp();
-    if (lane < NWP) s.chg[lane] = 0u;
-    int64_t nv[NW];
-    bool moved[NW];
+    int nc[NW], so[NW];
+    int64_t nv[NW], na[NW];
 #pragma unroll
     for (int r = 0; r < NW; ++r) {
       const int u = r * 32 + lane;
-      const int nc = (u < n && ((chg[r] >> lane) & 1u)) ? s.newcol[u] : rcol[r];
-      moved[r] = nc != rcol[r];
-      if (moved[r]) {
-        if (rcol[r] >= 0) {
-          work[(int64_t)u * n + rcol[r]] = mv[r];
-          const int so = aux_slot<NW>(s, u, rcol[r]);
-          if (so >= 0) s.auxl[so] = am[r];
-        }
-        rcol[r] = nc;
-        nv[r] = work[(int64_t)u * n + nc];
-        const int sn = aux_slot<NW>(s, u, nc);
-        am[r] = sn >= 0 ? s.auxl[sn] : 0;
-      }
+      nc[r] = u < n ? s.newcol[u] : -1;
     }
 #pragma unroll
-    for (int r = 0; r < NW; ++r)
-      if (moved[r]) mv[r] = nv[r];
+    for (int r = 0; r < NW; ++r) {
+      const int u = r * 32 + lane;
+      const bool moved = nc[r] != rcol[r];
+      const int sn = (moved && nc[r] >= alo[r] && nc[r] <= ahi[r]) ? abase[r] + nc[r] : -1;
+      so[r] = (moved && rcol[r] >= alo[r] && rcol[r] <= ahi[r]) ? abase[r] + rcol[r] : -1;
+      nv[r] = moved ? s.nvs[u] : mv[r];
+      na[r] = sn >= 0 ? s.auxl[sn] : (moved ? 0 : am[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < NW; ++r) {
+      const int u = r * 32 + lane;
+      if (nc[r] != rcol[r]) {
+        if (rcol[r] >= 0) work[(int64_t)u * n + rcol[r]] = mv[r];
+        if (so[r] >= 0) s.auxl[so[r]] = am[r];
+        rcol[r] = nc[r];
+        mv[r] = nv[r];
+        am[r] = na[r];
+      }
+    }
     __syncwarp();
     DPROF_T(t3);
     DPROF_ADD(3, t3 - t2);
