@@ -180,7 +180,16 @@ def bench_synth(args) -> dict:
                 "balance_kernel_gbs": round(alg["balance_kernel"] / (per["balance_kernel"] * 1e-3) / 1e9, 1),
                 "balance_kernel_frac": round(alg["balance_kernel"] / (per["balance_kernel"] * 1e-3) / 1e9 / hbm, 4),
                 "note": "decompose is a dependent chain of <= n^2-2n+2 peels per matrix "
-                        "(latency-bound); balance is the HBM-bound kernel"}
+                        "(latency-bound: one Kuhn re-augmentation of ~n/2 dependent "
+                        "shared-memory steps per peel); balance is the HBM-bound kernel"}
+    sm_hz = None
+    try:
+        sm_hz = torch.cuda.get_device_properties(0).clock_rate * 1e3
+    except Exception:
+        pass
+    if sm_hz:
+        peels = sum(n_raw) / len(n_raw)
+        roofline["decompose_cycles_per_peel"] = round(per["decompose_kernel"] * 1e-3 * sm_hz / peels, 1)
 
     # ---- e2e: host (pinned) D -> device -> synth -> packed schedule -> host,
     # through synthesize_host_batch (chunked, copies overlapped with kernels)

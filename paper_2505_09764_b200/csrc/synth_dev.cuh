@@ -419,33 +419,34 @@ __device__ __forceinline__ int dfs_warp(const DecSh<NW>& s, const int root) {
 
 // Apply an augmenting path (warp-wide): cm[pick[k]] = row_k where row_0 =
 // root and row_{k+1} = old cm[pick[k]]; record new columns, refresh supc.
-template <int NW>
-__device__ __forceinline__ void apply_path(const DecSh<NW>& s, const int root,
-                                           const int depth, const int lane,
-                                           const int64_t* work = nullptr, const int n = 0) {
-  constexpr int NWP = DecSh<NW>::NWP;
-  constexpr int J = (FAST_MAX_SERVERS + 31) / 32;
-  // an earlier path of this peel may still be filling nvs[] (same slots)
-  if (work) asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncwarp();  // lane 0's pick[] writes visible to the warp
-  const int jn = (depth >> 5) + 1;  // warp-uniform number of 32-element rounds
-  int rows[J], cols[J];
+// JN = number of 32-element rounds of the path (warp-uniform); within the
+// rounds everything is branch-free (clamped indices) so the loads of all
+// rounds issue back to back.
+template <int NW, int JN>
+__device__ __forceinline__ void apply_rounds(const DecSh<NW>& s, const int root, const int depth,
+                                             const int lane, const int64_t* work, const int n) {
+  constexpr int SH = DecSh<NW>::kRowShift;
+  int rows[JN], cols[JN];
+  bool act[JN];
 #pragma unroll
-  for (int j = 0; j < J; ++j) {
+  for (int j = 0; j < JN; ++j) {
     const int k = j * 32 + lane;
-    rows[j] = -1;
-    cols[j] = 0;
-    if (j < jn && k <= depth) {
-      cols[j] = s.pick[k] >> DecSh<NW>::kRowShift;
-      rows[j] = k == 0 ? root : s.cm[s.pick[k - 1] >> DecSh<NW>::kRowShift];
-    }
+    act[j] = k <= depth;
+    const int kk = act[j] ? k : depth;
+    cols[j] = s.pick[kk] >> SH;
+    rows[j] = s.pick[kk > 0 ? kk - 1 : 0] >> SH;  // column of the previous element
+  }
+#pragma unroll
+  for (int j = 0; j < JN; ++j) {
+    const int k = j * 32 + lane;
+    rows[j] = (k == 0 || !act[j]) ? root : s.cm[rows[j]];
   }
   __syncwarp();
 #pragma unroll
-  for (int j = 0; j < J; ++j) {
+  for (int j = 0; j < JN; ++j) {
     const int k = j * 32 + lane;
-    if (j < jn && k <= depth) {
-      const int v = cols[j], r = rows[j];
+    const int v = cols[j], r = rows[j];
+    if (act[j]) {
       // the row's new matched cell is read after the re-augmentation (peel
       // loop, "rows whose cell changed"): copy it into smem asynchronously
       if (work)
@@ -455,11 +456,29 @@ __device__ __forceinline__ void apply_path(const DecSh<NW>& s, const int root,
                      : "memory");
       s.cm[v] = (int16_t)r;
       s.newcol[r] = (int16_t)v;
-#pragma unroll
-      for (int w = 0; w < NWP; ++w) s.supc[v * NWP + w] = s.sup[r * NWP + w];
+      if constexpr (DecSh<NW>::NWP == 4) {
+        *reinterpret_cast<uint4*>(s.supc + v * 4) = *reinterpret_cast<const uint4*>(s.sup + r * 4);
+      } else {
+        *reinterpret_cast<uint2*>(s.supc + v * 2) = *reinterpret_cast<const uint2*>(s.sup + r * 2);
+      }
       if (k == depth) atomicAnd(&s.freeb[colword(v)], ~colbit(v));  // matched now
     }
   }
+}
+
+template <int NW>
+__device__ __forceinline__ void apply_path(const DecSh<NW>& s, const int root,
+                                           const int depth, const int lane,
+                                           const int64_t* work = nullptr, const int n = 0) {
+  // an earlier path of this peel may still be filling nvs[] (same slots)
+  if (work) asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncwarp();  // lane 0's pick[] writes visible to the warp
+  // path element k = j*32 + lane, k <= depth < n <= 32*NW
+  const int jn = depth >> 5;
+  if (jn == 0 || NW == 1) apply_rounds<NW, 1>(s, root, depth, lane, work, n);
+  else if (jn == 1 || NW == 2) apply_rounds<NW, (NW >= 2 ? 2 : 1)>(s, root, depth, lane, work, n);
+  else if (jn == 2 || NW == 3) apply_rounds<NW, (NW >= 3 ? 3 : 1)>(s, root, depth, lane, work, n);
+  else apply_rounds<NW, (NW >= 4 ? 4 : 1)>(s, root, depth, lane, work, n);
   __syncwarp();
 }
 
