@@ -686,39 +686,40 @@ __device__ void decompose_one(char* wsm, const int64_t* __restrict__ S_all, cons
     int src0 = -1, nfreed = 0, dst0 = 0;
 #pragma unroll
     for (int r = 0; r < NW; ++r) {
+      // rows u >= n carry mv = INT64_MAX - (sum of weights) > 0 and am = 0,
+      // so the arithmetic below is harmless for them; only stores are guarded
       const int u = r * 32 + lane;
-      bool real_pos = false, fr = false;
-      const int vsave = rcol[r];
-      if (u < n) {
-        const int v = rcol[r];
-        // strip_auxiliary (birkhoff.py:225-252): the cell pays aux first
-        const int64_t charged = am[r] < weight ? am[r] : weight;
-        const int64_t real = weight - charged;
-        am[r] -= charged;
-        mv[r] -= weight;
+      const bool valid = u < n;
+      const int v = rcol[r];
+      // strip_auxiliary (birkhoff.py:225-252): the cell pays aux first
+      const int64_t charged = am[r] < weight ? am[r] : weight;
+      const int64_t real = weight - charged;
+      am[r] -= charged;
+      mv[r] -= weight;
+      if (valid) {
         __stcs(bout + (int64_t)k * n + u, real);
         pout[(int64_t)k * n + u] = (uint8_t)v;
-        real_pos = real > 0;
-        if (mv[r] == 0) {
-          s.sup[u * NWP + colword(v)] &= ~colbit(v);
-          fr = remaining > 0;
-        }
       }
-      const uint32_t rb = __ballot_sync(0xffffffffu, real_pos);
+      const uint32_t rb = __ballot_sync(0xffffffffu, valid && real > 0);
+      const uint32_t zb = __ballot_sync(0xffffffffu, valid && mv[r] == 0);
       if (src0 < 0 && rb) {
         src0 = r * 32 + __ffs(rb) - 1;
-        dst0 = __shfl_sync(0xffffffffu, vsave, __ffs(rb) - 1);
+        dst0 = __shfl_sync(0xffffffffu, v, __ffs(rb) - 1);
       }
-      const uint32_t fb = __ballot_sync(0xffffffffu, fr);
-      if (fr) {
-        s.freed[nfreed + __popc(fb & ((1u << lane) - 1u))] = (int16_t)u;
-        s.cm[rcol[r]] = -1;  // unmatch (birkhoff.py:210-214)
+      if (zb) {  // warp-uniform: this round holds a peeled-out cell
+        if ((zb >> lane) & 1u) {
+          s.sup[u * NWP + colword(v)] &= ~colbit(v);
+          if (remaining > 0) {  // free the row (birkhoff.py:210-214)
+            s.freed[nfreed + __popc(zb & ((1u << lane) - 1u))] = (int16_t)u;
+            s.cm[v] = -1;
 #pragma unroll
-        for (int w = 0; w < NWP; ++w) s.supc[rcol[r] * NWP + w] = 0u;  // free: empty row
-        atomicOr(&s.freeb[colword(rcol[r])], colbit(rcol[r]));
-        rcol[r] = -1;
+            for (int w = 0; w < NWP; ++w) s.supc[v * NWP + w] = 0u;  // free: empty row
+            atomicOr(&s.freeb[colword(v)], colbit(v));
+            rcol[r] = -1;
+          }
+        }
+        if (remaining > 0) nfreed += __popc(zb);
       }
-      nfreed += __popc(fb);
     }
     if (lane == 0) {
       wout[k] = weight;
