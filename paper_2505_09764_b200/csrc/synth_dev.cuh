@@ -36,7 +36,8 @@ __host__ __device__ __forceinline__ int stage_cap(int n) {
 // Returns the number of moves, or -1 if an invariant breaks.
 template <int M>
 __device__ int balance_tile(int64_t* __restrict__ t, const int m_rt,
-                            fast_move* __restrict__ out, const int slots) {
+                            fast_move* __restrict__ out, const int slots,
+                            const int64_t* rowsum = nullptr) {
   constexpr int MM = M ? M : FAST_MAX_GPUS_PER_SERVER;
   const int m = M ? M : m_rt;
   int64_t dev[MM];
@@ -44,8 +45,13 @@ __device__ int balance_tile(int64_t* __restrict__ t, const int m_rt,
 #pragma unroll
   for (int p = 0; p < MM; ++p) {
     int64_t s = 0;
-    if (p < m)
-      for (int q = 0; q < m; ++q) s += t[p * m + q];
+    if (p < m) {
+      if (rowsum) {
+        s = rowsum[p];  // caller already summed the rows
+      } else {
+        for (int q = 0; q < m; ++q) s += t[p * m + q];
+      }
+    }
     dev[p] = s;
     total += s;
   }
