@@ -446,6 +446,13 @@ __device__ __forceinline__ void apply_rounds(const DecSh<NW>& s, const int root,
   for (int j = 0; j < JN; ++j) {
     const int k = j * 32 + lane;
     rows[j] = (k == 0 || !act[j]) ? root : s.cm[rows[j]];
+    // the row's new matched cell is read after the re-augmentation (peel
+    // loop, "rows whose cell changed"): start copying it into smem now
+    if (work && act[j])
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(s.nvs + rows[j])),
+                   "l"(work + (int64_t)rows[j] * n + cols[j])
+                   : "memory");
   }
   __syncwarp();
 #pragma unroll
@@ -453,13 +460,6 @@ __device__ __forceinline__ void apply_rounds(const DecSh<NW>& s, const int root,
     const int k = j * 32 + lane;
     const int v = cols[j], r = rows[j];
     if (act[j]) {
-      // the row's new matched cell is read after the re-augmentation (peel
-      // loop, "rows whose cell changed"): copy it into smem asynchronously
-      if (work)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(s.nvs + r)),
-                     "l"(work + (int64_t)r * n + v)
-                     : "memory");
       s.cm[v] = (int16_t)r;
       s.newcol[r] = (int16_t)v;
       if constexpr (DecSh<NW>::NWP == 4) {
@@ -760,10 +760,8 @@ __device__ void decompose_one(char* wsm, const int64_t* __restrict__ S_all, cons
     // (nvs, copied by apply_path) and aux_left, then write the old cell's
     // value and aux_left back.  Loads first, stores after: slots of distinct
     // cells never alias.
-    asm volatile("cp.async.wait_all;" ::: "memory");  // nvs[] from apply_path
-    __syncwarp();
     int nc[NW], so[NW];
-    int64_t nv[NW], na[NW];
+    int64_t na[NW];
 #pragma unroll
     for (int r = 0; r < NW; ++r) {
       const int u = r * 32 + lane;
@@ -771,11 +769,9 @@ __device__ void decompose_one(char* wsm, const int64_t* __restrict__ S_all, cons
     }
 #pragma unroll
     for (int r = 0; r < NW; ++r) {
-      const int u = r * 32 + lane;
       const bool moved = nc[r] != rcol[r];
       const int sn = (moved && nc[r] >= alo[r] && nc[r] <= ahi[r]) ? abase[r] + nc[r] : -1;
       so[r] = (moved && rcol[r] >= alo[r] && rcol[r] <= ahi[r]) ? abase[r] + rcol[r] : -1;
-      nv[r] = moved ? s.nvs[u] : mv[r];
       na[r] = sn >= 0 ? s.auxl[sn] : (moved ? 0 : am[r]);
     }
 #pragma unroll
@@ -784,8 +780,17 @@ __device__ void decompose_one(char* wsm, const int64_t* __restrict__ S_all, cons
       if (nc[r] != rcol[r]) {
         if (rcol[r] >= 0) work[(int64_t)u * n + rcol[r]] = mv[r];
         if (so[r] >= 0) s.auxl[so[r]] = am[r];
+      }
+    }
+    // the new cells' values (nvs, copied by apply_path) are needed last
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < NW; ++r) {
+      const int u = r * 32 + lane;
+      if (nc[r] != rcol[r]) {
         rcol[r] = nc[r];
-        mv[r] = nv[r];
+        mv[r] = s.nvs[u];
         am[r] = na[r];
       }
     }
