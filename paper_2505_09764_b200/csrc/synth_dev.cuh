@@ -354,13 +354,13 @@ __device__ __forceinline__ void load_row64(const uint32_t* src, uint64_t& r0, ui
   "mov.b32 %0, -1;\n\t"                                                 \
   "FDFS_END:\n\t"
 
+// Shared-window addresses are passed by value so that the DecSh of the
+// caller never escapes into this (non-inlined) call: otherwise its pointers
+// lose their shared address space and every later access becomes generic.
 template <int NW>
-__device__ __noinline__ int dfs_search(const DecSh<NW>& s, const int root) {
+__device__ __noinline__ int dfs_search(const uint32_t root_a, const uint32_t pick,
+                                       const uint32_t freeb, const uint32_t base) {
   constexpr int NWP = DecSh<NW>::NWP;
-  const uint32_t root_a = (uint32_t)__cvta_generic_to_shared(s.sup + root * NWP);
-  const uint32_t base = (uint32_t)__cvta_generic_to_shared(s.supc);
-  const uint32_t pick = (uint32_t)__cvta_generic_to_shared(s.pick);
-  const uint32_t freeb = (uint32_t)__cvta_generic_to_shared(s.freeb);
   int depth;
   if constexpr (NWP == 4) {
     asm volatile(
@@ -419,7 +419,11 @@ __device__ __noinline__ int dfs_search(const DecSh<NW>& s, const int root) {
 template <int NW>
 __device__ __forceinline__ int dfs_warp(const DecSh<NW>& s, const int root) {
   int depth = 0;
-  if ((threadIdx.x & 31) == 0) depth = dfs_search<NW>(s, root);
+  if ((threadIdx.x & 31) == 0)
+    depth = dfs_search<NW>((uint32_t)__cvta_generic_to_shared(s.sup + root * DecSh<NW>::NWP),
+                           (uint32_t)__cvta_generic_to_shared(s.pick),
+                           (uint32_t)__cvta_generic_to_shared(s.freeb),
+                           (uint32_t)__cvta_generic_to_shared(s.supc));
   return __shfl_sync(0xffffffffu, depth, 0);
 }
 
@@ -491,7 +495,7 @@ __device__ __forceinline__ void apply_path(const DecSh<NW>& s, const int root,
 // The whole decomposition of matrix b by one warp; `wsm` is this warp's
 // dec_smem_bytes_t<NW>(n) bytes of shared memory.
 template <int NW>
-__device__ void decompose_one(char* wsm, const int64_t* __restrict__ S_all, const int b,
+__device__ __forceinline__ void decompose_one(char* wsm, const int64_t* __restrict__ S_all, const int b,
                               const int n, const int mode, const int check_total,
                               const fast_sched_bufs& out, const int lane) {
   constexpr int NWP = DecSh<NW>::NWP;
