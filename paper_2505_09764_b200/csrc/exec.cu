@@ -294,9 +294,13 @@ __host__ __device__ inline size_t plan_smem_bytes(int n, int m) {
 // (`smem_ok`), else run on the global copies and the global workspace; the
 // whole CTA then builds the plan (plan_par.cuh).  Caller guarantees the
 // synthesis status is OK.
-__device__ void plan_cta(fastplan::PlanIn in, fastplan::PlanOut out, char* psm, int smem_ok) {
+// SMEM is a template parameter (not a runtime flag) so that, with the build
+// fully inlined, every staged pointer keeps the shared address space and the
+// plan runs on LDS/STS rather than generic loads.
+template <bool SMEM>
+__device__ __forceinline__ void plan_cta(fastplan::PlanIn in, fastplan::PlanOut out, char* psm) {
   void* ws = out.ws;
-  if (smem_ok) {
+  if constexpr (SMEM) {
     const int n = in.n, G = in.n * in.m, K = in.K;
     char* p = psm;
     ws = p; p += ((size_t)fastplan::par_ws_bytes(in.n, in.m, K) + 16 + 15) & ~(size_t)15;
@@ -338,7 +342,8 @@ __global__ void __launch_bounds__(kPlanThreads)
   }
   PLAN_STAMP(0);
   in.n_stages = *n_stages;
-  plan_cta(in, out, psm, smem_ok);
+  if (smem_ok) plan_cta<true>(in, out, psm);
+  else plan_cta<false>(in, out, psm);
 }
 
 // ---- fused single-launch path (n <= 6): everything before the exec loop ----
@@ -438,7 +443,7 @@ __device__ bool fused_prologue(const FusedArgs& f, uint8_t* const* peers, int ra
   in.perm = f.sched.stage_perm;
   in.sbytes = f.sched.stage_bytes;
   char* psm = dsm + ((dec_smem_bytes_t<1>(n) + 127) & ~(size_t)127);
-  plan_cta(in, out, psm, 1);
+  plan_cta<true>(in, out, psm);
   __threadfence();
   __syncthreads();
   return true;

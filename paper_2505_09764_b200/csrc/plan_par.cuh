@@ -154,7 +154,7 @@ __device__ __forceinline__ int64_t div_chunks(int64_t len, int64_t ch, int ch_sh
 // (bucket, pass) and its staging / flag-slot needs; EMIT = true: write the
 // ops.  Returns false when the window runs past the lane stream.
 template <bool EMIT>
-__device__ inline bool stage_window(const PlanIn& in, const ParWs& w, int s, int i, int p,
+__device__ __forceinline__ bool stage_window(const PlanIn& in, const ParWs& w, int s, int i, int p,
                                     fast_op* ops, int32_t op_base, int ch_shift) {
   const int n = in.n, m = in.m, G = n * m, K = in.K, MT = max_takes(m);
   const int k = in.order[s];
@@ -247,7 +247,7 @@ __device__ inline bool stage_window(const PlanIn& in, const ParWs& w, int s, int
 
 // Whole-CTA plan build.  `ws` holds par_ws_bytes(n, m, in.K); ops are written
 // to out.ops directly.  Every thread of the block must call it.
-__device__ inline void plan_compile_par(const PlanIn& in, const PlanOut& out, void* ws) {
+__device__ __forceinline__ void plan_compile_par(const PlanIn& in, const PlanOut& out, void* ws) {
   __shared__ int s_flags;
   __shared__ int32_t s_nbal, s_nint, s_nstage;
   const int n = in.n, m = in.m, G = n * m, T = n * (n - 1), K = in.K, MT = max_takes(m);
