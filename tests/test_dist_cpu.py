@@ -1,4 +1,5 @@
-"""Host-side logic of the multi-GPU path, world_size 2 on CPU (gloo).
+"""Host-side logic of the multi-GPU path on CPU (gloo): world_size 2 (2x1)
+and world_size 8 in the two partitions the 8-GPU runs use (2x4, 4x2).
 
 * count all-gather semantics: every rank assembles the same D (zero
   diagonal) and self-size vector from the per-rank rows;
@@ -25,7 +26,6 @@ import torch.multiprocessing as mp
 
 from conftest import REPO
 
-WORLD = 2
 
 
 def _free_port() -> int:
@@ -53,7 +53,7 @@ class _GlooComm:
         return recv
 
 
-def _worker(rank: int, port: int, errq):
+def _worker(rank: int, port: int, errq, WORLD: int, n: int, m: int):
     import sys
 
     sys.path.insert(0, REPO)
@@ -67,10 +67,10 @@ def _worker(rank: int, port: int, errq):
                                                     plan_compile_host)
         from paper_2505_09764_b200.schedule import PackedSchedule
 
-        n, m = 2, 1
         G = n * m
-        D = workloads.zipf_sizes(11, G, 1.2, 200_003)
-        selfb = np.array([777, 1234], dtype=np.int64)
+        assert G == WORLD
+        D = workloads.zipf_sizes(11, G, 1.2, 200_003 * G)
+        selfb = np.array([777 + 457 * g for g in range(G)], dtype=np.int64)
         Dfull = D + np.diag(selfb)
         # 1. count all-gather (mirrors gather_demand_kernel's layout)
         rows = [torch.zeros(G, dtype=torch.int64) for _ in range(G)]
@@ -114,7 +114,7 @@ def _worker(rank: int, port: int, errq):
         assert np.array_equal(recv[:lo], full[:lo])
         assert np.array_equal(recv[hi:len(full)], full[hi:])
         # 4. all_to_all_fast offset arithmetic vs all_to_all_single
-        splits = np.array([[3, 5], [4, 2]])
+        splits = np.random.default_rng(5).integers(0, 7, (G, G))
         x = torch.arange(int(splits[rank].sum()) * 6, dtype=torch.int32).reshape(-1, 6) + 1000 * rank
         y_fast = torch.zeros(int(splits[:, rank].sum()), 6, dtype=torch.int32)
         y_ref = torch.zeros_like(y_fast)
@@ -129,11 +129,13 @@ def _worker(rank: int, port: int, errq):
         raise
 
 
-def test_multi_rank_host_logic_gloo():
+@pytest.mark.parametrize("world,n,m", [(2, 2, 1), (8, 2, 4), (8, 4, 2)])
+def test_multi_rank_host_logic_gloo(world, n, m):
     ctx = mp.get_context("spawn")
     errq = ctx.SimpleQueue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, errq)) for r in range(WORLD)]
+    procs = [ctx.Process(target=_worker, args=(r, port, errq, world, n, m))
+             for r in range(world)]
     for pr in procs:
         pr.start()
     for pr in procs:
