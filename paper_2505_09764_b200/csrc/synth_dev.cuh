@@ -182,6 +182,7 @@ struct DecSh {
   int16_t* freed;  // [n]
   uint32_t* freeb; // [NWP] free columns (cm < 0), support-bitset layout
   int64_t* nvs;    // [n] value of a rematched row's new cell (cp.async'd in apply_path)
+  int64_t* wk;     // [n][n] the work matrix itself when NW == 1 (n <= 32), else unused
 };
 
 template <int NW>
@@ -194,6 +195,7 @@ __host__ __device__ __forceinline__ size_t dec_smem_bytes_t(int n) {
   b += 4 * (size_t)n * 2;                  // cm newcol pick freed
   b += NWP * 4 + 16;                       // freeb
   b += (size_t)n * 8;                      // nvs
+  if (NW == 1) b += (size_t)n * n * 8;     // wk: the work matrix (<= 8 KiB)
   return (b + 15) & ~(size_t)15;
 }
 
@@ -207,6 +209,7 @@ __device__ __forceinline__ DecSh<NW> dec_carve_t(char* p, int n) {
   s.C = (int64_t*)p; p += (size_t)(n + 1) * 8;
   s.auxl = (int64_t*)p; p += (size_t)(2 * n + 2) * 8;
   s.nvs = (int64_t*)p; p += (size_t)n * 8;
+  s.wk = (int64_t*)p; p += NW == 1 ? (size_t)n * n * 8 : 0;
   s.freeb = (uint32_t*)p; p += NWP * 4 + 16;
   s.cm = (int16_t*)p; p += n * 2;
   s.newcol = (int16_t*)p; p += n * 2;
@@ -501,8 +504,13 @@ __device__ __forceinline__ void decompose_one(char* wsm, const int64_t* __restri
   constexpr int NWP = DecSh<NW>::NWP;
   const int K = stage_cap(n);
   DecSh<NW> s = dec_carve_t<NW>(wsm, n);
-  int64_t* work = (int64_t*)((char*)out.workspace + (size_t)b * dec_ws_bytes_per_matrix(n));
-  uint64_t* key_w = (uint64_t*)(work + (size_t)n * n);
+  int64_t* const gwork =
+      (int64_t*)((char*)out.workspace + (size_t)b * dec_ws_bytes_per_matrix(n));
+  // n <= 32: the whole work matrix fits the warp's shared memory, so the
+  // rematched-cell reads of the peel loop never leave the SM
+  constexpr bool kSmemWork = NW == 1;
+  int64_t* const work = kSmemWork ? s.wk : gwork;
+  uint64_t* key_w = (uint64_t*)(gwork + (size_t)n * n);
   uint32_t* key_t = (uint32_t*)(key_w + K);
   const int64_t* S = S_all + (int64_t)b * n * n;
   int32_t* status = out.status + b;
@@ -752,7 +760,7 @@ __device__ __forceinline__ void decompose_one(char* wsm, const int64_t* __restri
       const int depth = dfs_warp<NW>(s, u);
       DPROF_T(tb);
       if (depth < 0) { st = FAST_EINVARIANT; break; }
-      apply_path<NW>(s, u, depth, lane, work, n);
+      apply_path<NW>(s, u, depth, lane, kSmemWork ? nullptr : work, n);
       DPROF_T(tc);
       DPROF_ADD(1, tb - ta);
       DPROF_ADD(2, tc - tb);
@@ -794,7 +802,7 @@ __device__ __forceinline__ void decompose_one(char* wsm, const int64_t* __restri
       const int u = r * 32 + lane;
       if (nc[r] != rcol[r]) {
         rcol[r] = nc[r];
-        mv[r] = s.nvs[u];
+        mv[r] = kSmemWork ? work[(int64_t)u * n + nc[r]] : s.nvs[u];
         am[r] = na[r];
       }
     }
