@@ -361,7 +361,7 @@ __device__ __forceinline__ void load_row64(const uint32_t* src, uint64_t& r0, ui
 // caller never escapes into this (non-inlined) call: otherwise its pointers
 // lose their shared address space and every later access becomes generic.
 template <int NW>
-__device__ __noinline__ int dfs_search(const uint32_t root_a, const uint32_t pick,
+__device__ __forceinline__ int dfs_search_body(const uint32_t root_a, const uint32_t pick,
                                        const uint32_t freeb, const uint32_t base) {
   constexpr int NWP = DecSh<NW>::NWP;
   int depth;
@@ -416,6 +416,22 @@ __device__ __noinline__ int dfs_search(const uint32_t root_a, const uint32_t pic
         : "memory");
   }
   return depth;
+}
+
+// Out-of-line copy for the wide rows (n > 64: long paths amortise the call,
+// and one copy of the loop keeps the kernel's code compact); n <= 64 inlines
+// the body at its call sites (short paths, the call overhead shows).
+template <int NW>
+__device__ __noinline__ int dfs_search_call(const uint32_t root_a, const uint32_t pick,
+                                            const uint32_t freeb, const uint32_t base) {
+  return dfs_search_body<NW>(root_a, pick, freeb, base);
+}
+
+template <int NW>
+__device__ __forceinline__ int dfs_search(const uint32_t root_a, const uint32_t pick,
+                                          const uint32_t freeb, const uint32_t base) {
+  if constexpr (NW >= 3) return dfs_search_call<NW>(root_a, pick, freeb, base);
+  else return dfs_search_body<NW>(root_a, pick, freeb, base);
 }
 
 // Lane 0 searches, the result is broadcast (the other lanes wait).
