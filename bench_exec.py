@@ -315,6 +315,33 @@ def run_moe(args) -> dict | None:
     ms = torch.tensor([t0.elapsed_time(t1) / args.steps], device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
+    # fused pack -> send (row-mapped executor source): same expert input, no
+    # packed send buffer written or read
+    fdisp = MoEDispatch(comm, T, RB, fused_pack=True)
+    frecv = fdisp.dispatch(tokens, seed=args.seed)
+    torch.cuda.synchronize()
+    comm.check()
+    okf = torch.tensor([0 if torch.equal(frecv[: nccl_out.numel()], nccl_out) else 1],
+                       device="cuda")
+    dist.all_reduce(okf)
+    if int(okf.item()) != 0:
+        raise RuntimeError("fused-pack MoE expert input differs from NCCL all_to_all_single")
+    for _ in range(args.warmup):
+        fdisp.dispatch(tokens, seed=args.seed)
+    torch.cuda.synchronize()
+    dist.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        fdisp.dispatch(tokens, seed=args.seed)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    comm.check()
+    fms = torch.tensor([f0.elapsed_time(f1) / args.steps], device="cuda")
+    dist.all_reduce(fms, op=dist.ReduceOp.MAX)
+    fms = float(fms.item())
+    disp.dispatch(tokens, seed=args.seed)  # the combine below uses disp's forward state
+    torch.cuda.synchronize()
     # NCCL path: our route + pack, NCCL alltoall (no FAST), timed the same way
     for _ in range(args.warmup):
         disp.route(args.seed)
@@ -370,6 +397,11 @@ def run_moe(args) -> dict | None:
                           "bottleneck_gpu_bytes": bn},
                "t_roof_us": round(bn / (PEER_GBS * 1e9) * 1e6, 1),
                "frac_of_alltoallv_roofline": round(bn / (PEER_GBS * 1e9) / (ms * 1e-3), 4),
+               "fused_pack": {"ms": round(fms, 4),
+                              "value": round(T * world / (fms * 1e-3), 1), "unit": "tokens/s",
+                              "what": "dispatch with the pack fused into the executor's "
+                                      "source reads (row map, no send buffer)",
+                              "parity": "expert input == NCCL all_to_all_single"},
                "combine_ms": round(cms, 4),
                "layer_dispatch_plus_combine_ms": round(ms + cms, 4),
                "nccl_path": {"ms": round(nms, 4),

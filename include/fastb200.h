@@ -272,6 +272,15 @@ int fast_alltoallv(fast_comm *c, const void *send, const int64_t *counts, int n,
  * is the multi-launch path (measured equal or faster on B200, see
  * profiles/README.md). */
 int fast_comm_set_fused(fast_comm *c, int enable);
+/* Fused MoE pack -> send: while set, the executor
+ * reads every SEND byte through a row map instead of a packed send buffer:
+ * virtual send row r is row row_src[r] of rows_base (row_bytes each, 16-byte
+ * multiple; n_rows virtual rows, n_rows * row_bytes / 16 < 2^32).  The send
+ * pointer passed to fast_exec / fast_alltoallv is then ignored for data.
+ * Launch arguments are taken at enqueue time; row_src == NULL clears it. */
+int fast_comm_set_send_rows(fast_comm *c, const void *rows_base,
+                            const int32_t *row_src, int64_t row_bytes,
+                            int64_t n_rows);
 /* Number of calls issued through fast_alltoallv (the current epoch); callers
  * that drive fast_gather_demand / fast_exec themselves report theirs with
  * fast_comm_set_epoch so both paths share one monotone counter. */
@@ -328,6 +337,19 @@ int fast_moe_pack(const void *tokens, int T, int k, int64_t row_bytes,
  * self_bytes are the gathered demand matrix / self sizes of the call. */
 int fast_moe_unpack_self(const int64_t *D, const int64_t *self_bytes, int G,
                          int rank, const void *send, void *recv, void *stream);
+
+/* Fused pack (with fast_comm_set_send_rows): row_src[row] = t for each of
+ * the T*k send rows fast_moe_pack would write, i.e. its destination map
+ * inverted; 4 bytes per row instead of row_bytes. */
+int fast_moe_rowmap(int T, int k, const int32_t *topk, const int32_t *pos,
+                    const void *workspace, int E, const int64_t *seg_rows,
+                    int32_t *row_src, void *stream);
+/* fast_moe_unpack_self for the row-mapped send: the own segment's rows are
+ * read from `tokens` through row_src. */
+int fast_moe_unpack_self_rows(const int64_t *D, const int64_t *self_bytes,
+                              int G, int rank, const void *tokens,
+                              const int32_t *row_src, int64_t row_bytes,
+                              void *recv, void *stream);
 
 /* Combine (the second alltoallv of an MoE layer,
  * PAPER.md:120): after the reverse FAST alltoallv (counts = column `rank` of

@@ -113,6 +113,14 @@ struct ExecArgs {
   int64_t* timeline;
   int rank, world;
   int skip_barrier;  // caller already synchronised the ranks for this epoch
+  // fused pack -> send (fast_comm_set_send_rows): when row_src is set, SEND
+  // offsets are virtual; virtual row r is row row_src[r] of rows_base
+  const uint8_t* rows_base;
+  const int32_t* row_src;
+  uint32_t row_vec, row_magic;  // row_bytes / 16; udiv magic for it
+  int row_l;                    // ceil(log2(row_vec))
+  const uint8_t* rows_bases[kMaxRanks];  // group mode: per local rank slot
+  const int32_t* row_srcs[kMaxRanks];
 };
 
 __device__ __forceinline__ uint64_t* ctr(uint8_t* base, int idx) {
@@ -195,6 +203,66 @@ __device__ void cta_copy(uint8_t* dst, const uint8_t* src, int64_t len, bool nc)
   }
   const int64_t tail = len - nw * 16;
   if (tid < tail) dst[nw * 16 + tid] = src[nw * 16 + tid];
+}
+
+// ---- row-mapped source (fused MoE pack -> lane send) ------------------------
+// Virtual send word vw (16 B) lies in virtual row q = vw / row_vec, which is
+// token row row_src[q]; the division is Granlund-Montgomery (exact for every
+// u32 vw), so the per-word cost is one umulhi and an L1-resident index load.
+__device__ __forceinline__ const uint8_t* vword(const ExecArgs& a, uint32_t vw) {
+  uint32_t q = vw;
+  if (a.row_vec > 1) {
+    const uint32_t t = __umulhi(vw, a.row_magic);
+    q = (t + ((vw - t) >> 1)) >> (a.row_l - 1);
+  }
+  const uint32_t r = vw - q * a.row_vec;
+  return a.rows_base + ((int64_t)__ldg(a.row_src + q) * a.row_vec + r) * 16;
+}
+
+// cta_copy with the source bytes [vsrc, vsrc + len) of the virtual send buffer
+__device__ void cta_copy_rows(uint8_t* dst, int64_t vsrc, int64_t len, const ExecArgs& a) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  int64_t head = (16 - ((uintptr_t)dst & 15)) & 15;
+  if (head > len) head = len;
+  if (tid < head) dst[tid] = vword(a, (uint32_t)((vsrc + tid) >> 4))[(vsrc + tid) & 15];
+  dst += head;
+  vsrc += head;
+  len -= head;
+  const int64_t nw = len >> 4;
+  const int sh = (int)(vsrc & 15);
+  const uint32_t w0 = (uint32_t)(vsrc >> 4);
+  constexpr int U = FAST_COPY_UNROLL;
+  if (sh == 0) {
+    int64_t wi = tid;
+    for (; wi + (U - 1) * nt < nw; wi += U * nt) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ld16(vword(a, w0 + (uint32_t)(wi + u * nt)), true);
+#pragma unroll
+      for (int u = 0; u < U; ++u) st16(dst + (wi + u * nt) * 16, v[u]);
+    }
+    for (; wi < nw; wi += nt) st16(dst + wi * 16, ld16(vword(a, w0 + (uint32_t)wi), true));
+  } else {
+    int64_t wi = tid;
+    for (; wi + (U - 1) * nt < nw; wi += U * nt) {
+      uint4 x[U], y[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        x[u] = ld16(vword(a, w0 + (uint32_t)(wi + u * nt)), true);
+        y[u] = ld16(vword(a, w0 + (uint32_t)(wi + u * nt) + 1), true);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) st16(dst + (wi + u * nt) * 16, shift_window(x[u], y[u], sh));
+    }
+    for (; wi < nw; wi += nt)
+      st16(dst + wi * 16, shift_window(ld16(vword(a, w0 + (uint32_t)wi), true),
+                                       ld16(vword(a, w0 + (uint32_t)wi + 1), true), sh));
+  }
+  const int64_t tail = len - nw * 16;
+  if (tid < tail) {
+    const int64_t v = vsrc + nw * 16 + tid;
+    dst[nw * 16 + tid] = vword(a, (uint32_t)(v >> 4))[v & 15];
+  }
 }
 
 // ---- kernels ----------------------------------------------------------------
@@ -459,6 +527,10 @@ __global__ void __launch_bounds__(kExecThreads) exec_kernel(ExecArgs a, FusedArg
   extern __shared__ __align__(16) char fsm[];
   a.rank += blockIdx.y;
   a.send = a.sends[blockIdx.y];
+  if (a.row_srcs[blockIdx.y]) {
+    a.rows_base = a.rows_bases[blockIdx.y];
+    a.row_src = a.row_srcs[blockIdx.y];
+  }
   if (a.timeline) a.timeline += (int64_t)blockIdx.y * kTimelineStride;
   uint8_t* me = a.peers[a.rank];
   uint64_t* status = ctr(me, CTR_STATUS);
@@ -565,7 +637,10 @@ __global__ void __launch_bounds__(kExecThreads) exec_kernel(ExecArgs a, FusedArg
       __syncthreads();
       if (s_fail) break;
     }
-    cta_copy(dst + off, src + off, len, o.src_buf == FAST_BUF_SEND);
+    if (o.src_buf == FAST_BUF_SEND && a.row_src)
+      cta_copy_rows(dst + off, o.src_off + off, len, a);
+    else
+      cta_copy(dst + off, src + off, len, o.src_buf == FAST_BUF_SEND);
     __syncthreads();
     if (tid == 0) {
       __threadfence_system();
@@ -597,7 +672,20 @@ struct fast_comm {
   int opened;
   int64_t epoch;  // calls issued through fast_alltoallv
   int no_fuse;    // 1: always use the multi-launch path
+  // fast_comm_set_send_rows state (row_src == nullptr: plain send buffer)
+  const uint8_t* rows_base;
+  const int32_t* row_src;
+  uint32_t row_vec, row_magic;
+  int row_l;
 };
+
+static void set_rowmap(ExecArgs& a, const fast_comm* c) {
+  a.rows_base = c->rows_base;
+  a.row_src = c->row_src;
+  a.row_vec = c->row_vec;
+  a.row_magic = c->row_magic;
+  a.row_l = c->row_l;
+}
 
 extern "C" {
 
@@ -833,6 +921,7 @@ static int exec_launch(fast_comm* c, const fast_plan* plan, const void* send, in
   a.rank = c->rank;
   a.world = c->world;
   a.skip_barrier = skip_barrier;
+  set_rowmap(a, c);
   FusedArgs f;
   memset(&f, 0, sizeof(f));
   exec_kernel<false><<<blocks, kExecThreads, 0, (cudaStream_t)stream>>>(a, f);
@@ -872,7 +961,16 @@ int fast_exec_group(fast_comm* const* comms, int world, const fast_plan* plan,
   a.ops = plan->ops;
   a.n_ops = plan->n_ops;
   a.plan_status = plan->status;
-  for (int r = 0; r < world; ++r) a.sends[r] = (const uint8_t*)sends[r];
+  for (int r = 0; r < world; ++r) {
+    a.sends[r] = (const uint8_t*)sends[r];
+    if (!comms[r]->row_src) continue;
+    if (a.row_vec && a.row_vec != comms[r]->row_vec) return FAST_EVALIDATION;
+    a.rows_bases[r] = comms[r]->rows_base;
+    a.row_srcs[r] = comms[r]->row_src;
+    a.row_vec = comms[r]->row_vec;
+    a.row_magic = comms[r]->row_magic;
+    a.row_l = comms[r]->row_l;
+  }
   a.recv_off = comms[0]->recv_off;
   a.staging_off = comms[0]->staging_off;
   a.chunk = chunk_bytes & ~(int64_t)15;
@@ -942,6 +1040,7 @@ static int launch_fused(fast_comm* c, const void* send, const int64_t* counts, i
   a.rank = c->rank;
   a.world = c->world;
   a.skip_barrier = 1;  // the in-kernel demand all-gather synchronises the ranks
+  set_rowmap(a, c);
   FusedArgs f;
   memset(&f, 0, sizeof(f));
   f.counts = counts;
@@ -995,6 +1094,29 @@ int fast_alltoallv(fast_comm* c, const void* send, const int64_t* counts, int n,
                          c->staging_bytes, chunk_bytes, plan, stream);
   if (rc != FAST_OK) return rc;
   return exec_launch(c, plan, send, 0, blocks, chunk_bytes, timeline_ns, stream, 1);
+}
+
+int fast_comm_set_send_rows(fast_comm* c, const void* rows_base, const int32_t* row_src,
+                            int64_t row_bytes, int64_t n_rows) {
+  if (!c) return FAST_EVALIDATION;
+  if (!row_src) {
+    c->rows_base = nullptr;
+    c->row_src = nullptr;
+    return FAST_OK;
+  }
+  if (!rows_base || row_bytes < 16 || (row_bytes & 15) || ((uintptr_t)rows_base & 15) ||
+      n_rows < 0 || row_bytes / 16 > 0xffffffffll ||
+      (n_rows * (row_bytes / 16)) >= ((int64_t)1 << 32))
+    return FAST_EVALIDATION;
+  const uint32_t d = (uint32_t)(row_bytes / 16);
+  int l = 0;
+  while (((uint64_t)1 << l) < d) ++l;
+  c->rows_base = (const uint8_t*)rows_base;
+  c->row_src = row_src;
+  c->row_vec = d;
+  c->row_l = l;
+  c->row_magic = d > 1 ? (uint32_t)((((uint64_t)1 << 32) * (((uint64_t)1 << l) - d)) / d + 1) : 0;
+  return FAST_OK;
 }
 
 int64_t fast_comm_epoch(const fast_comm* c) { return c ? c->epoch : -1; }

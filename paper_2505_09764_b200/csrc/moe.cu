@@ -166,6 +166,43 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// fused pack -> send: instead of materialising the send buffer, record for
+// every send row the token it holds (row_src[row] = t, the pack kernel's
+// destination map inverted); the executor then reads token rows through it
+template <int K>
+__global__ void moe_rowmap_kernel(int T, const int32_t* __restrict__ topk,
+                                  const int32_t* __restrict__ pos,
+                                  const int32_t* __restrict__ blkbase, int E,
+                                  const int64_t* __restrict__ seg_rows,
+                                  int32_t* __restrict__ row_src) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < T * K; i += gridDim.x * blockDim.x) {
+    const int e = topk[i];
+    row_src[seg_rows[e] + blkbase[(int64_t)(i / kRouteThreads) * E + e] + pos[i]] = i / K;
+  }
+}
+
+// own segment of the virtual send buffer (rows row_src[s0 ...]) -> the self
+// slot of the receive buffer; one warp per row
+__global__ void moe_unpack_self_rows_kernel(const int64_t* __restrict__ D,
+                                            const int64_t* __restrict__ self_bytes, int G,
+                                            int rank, const uint4* __restrict__ tokens,
+                                            const int32_t* __restrict__ row_src, int64_t row_vec,
+                                            uint8_t* __restrict__ recv) {
+  int64_t soff = 0, roff = 0;
+  for (int h = 0; h < rank; ++h) soff += D[(int64_t)rank * G + h];
+  for (int g = 0; g < rank; ++g) roff += D[(int64_t)g * G + rank];
+  const int64_t RB = row_vec * 16;
+  const int64_t s0 = soff / RB, nrows = self_bytes[rank] / RB;
+  uint4* d = reinterpret_cast<uint4*>(recv + roff);
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < nrows; r += nwarps) {
+    const uint4* src = tokens + (int64_t)row_src[s0 + r] * row_vec;
+    for (int64_t v = lane; v < row_vec; v += 32) stg_na(d + r * row_vec + v, ldg_nc(src + v));
+  }
+}
+
 // own segment: send[sum_{h<rank} D[rank][h] ...] -> recv[sum_{g<rank} D[g][rank] ...]
 __global__ void moe_unpack_self_kernel(const int64_t* __restrict__ D,
                                        const int64_t* __restrict__ self_bytes, int G, int rank,
@@ -332,6 +369,38 @@ int fast_moe_unpack_self(const int64_t* D, const int64_t* self_bytes, int G, int
     return FAST_EVALIDATION;
   moe_unpack_self_kernel<<<2 * sm_count(), 512, 0, (cudaStream_t)stream>>>(
       D, self_bytes, G, rank, (const uint8_t*)send, (uint8_t*)recv);
+  return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
+}
+
+int fast_moe_rowmap(int T, int k, const int32_t* topk, const int32_t* pos,
+                    const void* workspace, int E, const int64_t* seg_rows, int32_t* row_src,
+                    void* stream) {
+  if (T < 0 || (k != 1 && k != 2 && k != 4 && k != 8) || E < 1 || E > kMaxExperts || !topk ||
+      !pos || !workspace || !seg_rows || !row_src)
+    return FAST_EVALIDATION;
+  if (T == 0) return FAST_OK;
+  const int64_t N = (int64_t)T * k;
+  int blocks = (int)((N + 255) / 256);
+  if (blocks > 4 * sm_count()) blocks = 4 * sm_count();
+  cudaStream_t s = (cudaStream_t)stream;
+  const int32_t* bb = (const int32_t*)workspace;
+  switch (k) {
+    case 1: moe_rowmap_kernel<1><<<blocks, 256, 0, s>>>(T, topk, pos, bb, E, seg_rows, row_src); break;
+    case 2: moe_rowmap_kernel<2><<<blocks, 256, 0, s>>>(T, topk, pos, bb, E, seg_rows, row_src); break;
+    case 4: moe_rowmap_kernel<4><<<blocks, 256, 0, s>>>(T, topk, pos, bb, E, seg_rows, row_src); break;
+    default: moe_rowmap_kernel<8><<<blocks, 256, 0, s>>>(T, topk, pos, bb, E, seg_rows, row_src); break;
+  }
+  return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
+}
+
+int fast_moe_unpack_self_rows(const int64_t* D, const int64_t* self_bytes, int G, int rank,
+                              const void* tokens, const int32_t* row_src, int64_t row_bytes,
+                              void* recv, void* stream) {
+  if (!D || !self_bytes || G < 1 || rank < 0 || rank >= G || !tokens || !row_src || !recv ||
+      row_bytes <= 0 || (row_bytes & 15) || ((uintptr_t)tokens & 15) || ((uintptr_t)recv & 15))
+    return FAST_EVALIDATION;
+  moe_unpack_self_rows_kernel<<<2 * sm_count(), 512, 0, (cudaStream_t)stream>>>(
+      D, self_bytes, G, rank, (const uint4*)tokens, row_src, row_bytes / 16, (uint8_t*)recv);
   return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
 }
 

@@ -188,13 +188,36 @@ class FastComm:
 
     def alltoallv(self, send: torch.Tensor, send_counts: torch.Tensor,
                   stream: torch.cuda.Stream | None = None, record_timeline: bool = False,
-                  exec_events: tuple | None = None) -> torch.Tensor:
+                  exec_events: tuple | None = None,
+                  send_rows: tuple | None = None) -> torch.Tensor:
         """FAST alltoallv of `send` (uint8, device) split by send_counts
         (int64[world] device, bytes per destination in send order; the own
         entry is the self segment, which stays in place and is not moved).
         Returns the recv region: source-major segments exactly like
         all_to_all_single's output, except that the own segment's slot is a
-        gap of send_counts[rank] bytes (never transferred; fill it locally)."""
+        gap of send_counts[rank] bytes (never transferred; fill it locally).
+
+        send_rows = (rows, row_src, row_bytes): the send buffer is virtual,
+        its row r being row row_src[r] of `rows` (fused MoE pack -> send,
+        fast_comm_set_send_rows); `send` is then only a placeholder."""
+        lib = _lib.load()
+        if send_rows is None:
+            return self._alltoallv(send, send_counts, stream, record_timeline, exec_events)
+        rows, row_src, row_bytes = send_rows
+        if row_src.dtype != torch.int32 or not row_src.is_cuda or not rows.is_cuda:
+            raise ValidationError("send_rows: rows / row_src (int32) must be cuda tensors")
+        _lib.check_rc(lib.fast_comm_set_send_rows(self._ptr, ctypes.c_void_p(rows.data_ptr()),
+                                                  ctypes.c_void_p(row_src.data_ptr()),
+                                                  int(row_bytes), row_src.numel()),
+                      "fast_comm_set_send_rows")
+        try:
+            return self._alltoallv(send, send_counts, stream, record_timeline, exec_events,
+                                   (rows.data_ptr(), row_src.data_ptr(), int(row_bytes)))
+        finally:
+            lib.fast_comm_set_send_rows(self._ptr, None, None, 0, 0)
+
+    def _alltoallv(self, send, send_counts, stream, record_timeline, exec_events,
+                   rows_key=None) -> torch.Tensor:
         lib = _lib.load()
         if send.dtype != torch.uint8 or not send.is_cuda:
             raise ValidationError("send must be a cuda uint8 tensor")
@@ -206,7 +229,7 @@ class FastComm:
         s = stream or torch.cuda.current_stream()
         tl = ctypes.c_void_p(self.timeline.data_ptr()) if record_timeline else None
         if exec_events is None:
-            key = (send.data_ptr(), row.data_ptr(), bool(record_timeline), self._fused)
+            key = (send.data_ptr(), row.data_ptr(), bool(record_timeline), self._fused, rows_key)
             g = self._graphs.get(key) if (self.use_graph and stream is None) else None
             if g is not None:  # one graph launch per call
                 g.replay()
@@ -360,11 +383,25 @@ class GroupComm:
 
     def alltoallv(self, sends: list[torch.Tensor], D: torch.Tensor,
                   stream: torch.cuda.Stream | None = None,
-                  self_bytes: torch.Tensor | None = None) -> list[torch.Tensor]:
+                  self_bytes: torch.Tensor | None = None,
+                  send_rows: list | None = None) -> list[torch.Tensor]:
         """D: [world, world] int64, zero diagonal.  self_bytes (optional,
         int64[world]): own segments kept in place in send_g and left as a
-        gap in recv_g (all_to_all_single layout)."""
+        gap in recv_g (all_to_all_single layout).  send_rows (optional, per
+        rank (rows, row_src, row_bytes)): row-mapped send buffers, as in
+        FastComm.alltoallv."""
         lib = _lib.load()
+        if send_rows is not None:
+            for r, (rows, row_src, rb) in enumerate(send_rows):
+                _lib.check_rc(lib.fast_comm_set_send_rows(
+                    self._ptrs[r], ctypes.c_void_p(rows.data_ptr()),
+                    ctypes.c_void_p(row_src.data_ptr()), int(rb), row_src.numel()),
+                    "fast_comm_set_send_rows")
+            try:
+                return self.alltoallv(sends, D, stream, self_bytes)
+            finally:
+                for r in range(self.world):
+                    lib.fast_comm_set_send_rows(self._ptrs[r], None, None, 0, 0)
         n, m = self.topology.n_servers, self.topology.gpus_per_server
         if D.dtype != torch.int64 or tuple(D.shape) != (self.world, self.world):
             raise ValidationError("D must be int64 [world, world]")

@@ -39,7 +39,7 @@ class MoEDispatch:
     """Device buffers + the five kernels of one MoE dispatch (one rank)."""
 
     def __init__(self, comm, tokens_per_gpu: int, row_bytes: int, k: int = 2,
-                 alpha: float = 0.8):
+                 alpha: float = 0.8, fused_pack: bool = False):
         if row_bytes % 16:
             raise ValidationError("row_bytes must be a multiple of 16")
         if k != 2:
@@ -56,7 +56,12 @@ class MoEDispatch:
         self.demand_row = torch.empty(self.E, dtype=torch.int64, device=dev)
         self.ws = torch.empty(max(16, int(lib.fast_moe_route_workspace_bytes(self.T, k, self.E))),
                               dtype=torch.uint8, device=dev)
-        self.send = torch.empty(self.T * k * row_bytes, dtype=torch.uint8, device=dev)
+        # fused_pack: the executor reads token rows through row_src (4 B per
+        # send row) and the packed send buffer is never written
+        self.fused_pack = fused_pack
+        self.row_src = torch.empty(self.T * k, dtype=torch.int32, device=dev)
+        self.send = torch.empty(0 if fused_pack else self.T * k * row_bytes, dtype=torch.uint8,
+                                device=dev)
         self.set_hot(0, alpha)
 
     def set_hot(self, hot: int, alpha: float = 0.8) -> None:
@@ -85,6 +90,20 @@ class MoEDispatch:
                                         P(self.pos), P(self.ws), self.E, P(self.seg_rows),
                                         P(self.send), _stream_handle(stream)), "fast_moe_pack")
 
+    def rowmap(self, stream=None, tokens: torch.Tensor | None = None) -> None:
+        """row_src[send row] = token (fast_moe_rowmap): the pack's
+        destination map inverted, for the fused pack -> send.  `tokens`
+        (kept for unpack) defaults to the last dispatch's."""
+        lib = _lib.load()
+        if tokens is not None:
+            if tokens.numel() * tokens.element_size() != self.T * self.row_bytes:
+                raise ValidationError("tokens must be [T, row_bytes] worth of data")
+            self._tokens = tokens.contiguous().view(torch.uint8).reshape(-1)
+        P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        _lib.check_rc(lib.fast_moe_rowmap(self.T, self.k, P(self.topk), P(self.pos), P(self.ws),
+                                          self.E, P(self.seg_rows), P(self.row_src),
+                                          _stream_handle(stream)), "fast_moe_rowmap")
+
     def unpack(self, stream=None, D: torch.Tensor | None = None,
                self_sizes: torch.Tensor | None = None, recv: torch.Tensor | None = None
                ) -> torch.Tensor:
@@ -95,6 +114,14 @@ class MoEDispatch:
         D = c.demand() if D is None else D
         ss = c.self_sizes() if self_sizes is None else self_sizes
         recv = c.recv if recv is None else recv
+        if self.fused_pack:
+            P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+            _lib.check_rc(lib.fast_moe_unpack_self_rows(P(D), P(ss), c.world, c.rank,
+                                                        P(self._tokens), P(self.row_src),
+                                                        self.row_bytes, P(recv),
+                                                        _stream_handle(stream)),
+                          "fast_moe_unpack_self_rows")
+            return recv
         _lib.check_rc(lib.fast_moe_unpack_self(ctypes.c_void_p(D.data_ptr()),
                                                ctypes.c_void_p(ss.data_ptr()), c.world, c.rank,
                                                ctypes.c_void_p(self.send.data_ptr()),
@@ -106,8 +133,13 @@ class MoEDispatch:
         """Full dispatch; returns the receive region (expert input rows,
         source-major; the row count is counts summed over sources)."""
         self.route(seed, stream)
-        self.pack(tokens, stream)
-        self.comm.alltoallv(self.send, self.demand_row, stream=stream)
+        if self.fused_pack:
+            self.rowmap(stream, tokens)
+            self.comm.alltoallv(self._tokens, self.demand_row, stream=stream,
+                                send_rows=(self._tokens, self.row_src, self.row_bytes))
+        else:
+            self.pack(tokens, stream)
+            self.comm.alltoallv(self.send, self.demand_row, stream=stream)
         self.remember_forward(self.comm.demand(), self.comm.self_sizes())
         return self.unpack(stream)
 

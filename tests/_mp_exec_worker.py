@@ -97,6 +97,18 @@ def main() -> int:
         if not np.array_equal(got, want):
             print(f"[rank {rank}] MoE expert input mismatch (n={n}, m={m})", flush=True)
             ok = False
+        # fused pack -> send: the executor reads token rows through row_src
+        fdisp = MoEDispatch(mcomm, T, RB, fused_pack=True)
+        for rep in range(2):  # second call replays the captured graph
+            frecv = fdisp.dispatch(torch.from_numpy(toks[rank]).cuda(), seed=1)
+            torch.cuda.synchronize()
+            mcomm.check()
+            if not np.array_equal(frecv[: want.size].cpu().numpy().reshape(-1, RB), want):
+                print(f"[rank {rank}] fused-pack MoE expert input mismatch (n={n}, m={m}, "
+                      f"call {rep})", flush=True)
+                ok = False
+        recv = disp.dispatch(torch.from_numpy(toks[rank]).cuda(), seed=1)  # restore disp's state
+        torch.cuda.synchronize()
         # combine: experts scale by 2^rank (exact), reverse FAST alltoallv, weighted sum
         n_in = want.size
         expert_out = torch.zeros(2 * T * RB * 3, dtype=torch.uint8, device="cuda")

@@ -75,7 +75,74 @@ def test_moe_dispatch_group_mode_matches_oracle():
         n = want[h].shape[0] * RB
         got = recvs[h][:n].cpu().numpy().reshape(-1, RB)
         assert np.array_equal(got, want[h]), h
+    # fused pack -> send: no send buffer; the executor reads token rows
+    # through row_src (fast_comm_set_send_rows), same expert inputs
+    for r in recvs:
+        r.fill_(0xA5)
+    fdisps, srows, toks_dev = [], [], []
+    for s in range(G):
+        d = MoEDispatch(GroupRank(group, s), T, RB, fused_pack=True)
+        tk = torch.from_numpy(tokens_np[s]).cuda()
+        d.route(seed)
+        d.rowmap(tokens=tk)
+        fdisps.append(d)
+        toks_dev.append(tk)
+        srows.append((d._tokens, d.row_src, RB))
+    torch.cuda.synchronize()
+    for s, d in enumerate(fdisps):
+        _, seg, _ = moe_oracle.route(topks[s], G)
+        packed = moe_oracle.pack(tokens_np[s], topks[s], G)
+        rs = d.row_src.cpu().numpy()
+        assert np.array_equal(tokens_np[s][rs], packed), s  # row map == pack order
+    recvs = group.alltoallv([t.view(torch.uint8).reshape(-1) for t in toks_dev], D,
+                            self_bytes=selfb, send_rows=srows)
+    for s, d in enumerate(fdisps):
+        d.unpack(D=D, self_sizes=selfb, recv=recvs[s])
+    torch.cuda.synchronize()
+    group.check()
+    for h in range(G):
+        n = want[h].shape[0] * RB
+        got = recvs[h][:n].cpu().numpy().reshape(-1, RB)
+        assert np.array_equal(got, want[h]), ("fused", h)
     group.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("RB", [48, 1040, 4112])
+def test_fused_pack_odd_row_sizes_group_mode(RB):
+    """Row-mapped send with row_bytes not a power of two (the executor's
+    u32 magic division) and FAST's byte-granular splits crossing rows: the
+    fused and the packed dispatch give identical expert inputs."""
+    from paper_2505_09764_b200 import Topology
+    from paper_2505_09764_b200.executor import GroupComm, GroupRank
+    from paper_2505_09764_b200.moe import MoEDispatch
+
+    G, T, seed = 4, 1500, 9
+    toks = [torch.from_numpy(payload(300 + s, T * RB).reshape(T, RB)).cuda() for s in range(G)]
+    cap = 2 * T * RB * 4
+    outs = {}
+    for fused in (False, True):
+        group = GroupComm(Topology(2, 2), recv_bytes=cap, staging_bytes=cap, blocks=8,
+                          chunk_bytes=4096 + 16 * 3)
+        ds = [MoEDispatch(GroupRank(group, s), T, RB, fused_pack=fused) for s in range(G)]
+        for s, d in enumerate(ds):
+            d.route(seed)
+            d.rowmap(tokens=toks[s]) if fused else d.pack(toks[s])
+        Dfull = torch.stack([d.demand_row for d in ds])
+        selfb = torch.diagonal(Dfull).clone()
+        D = Dfull.clone()
+        D.fill_diagonal_(0)
+        sends = [t.view(torch.uint8).reshape(-1) for t in toks] if fused else [d.send for d in ds]
+        rows = [(d._tokens, d.row_src, RB) for d in ds] if fused else None
+        recvs = group.alltoallv(sends, D, self_bytes=selfb, send_rows=rows)
+        for s, d in enumerate(ds):
+            d.unpack(D=D, self_sizes=selfb, recv=recvs[s])
+        torch.cuda.synchronize()
+        group.check()
+        outs[fused] = [recvs[h][: int(Dfull[:, h].sum())].cpu().numpy() for h in range(G)]
+        group.close()
+    for h in range(G):
+        assert np.array_equal(outs[True][h], outs[False][h]), h
 
 
 @pytest.mark.gpu
