@@ -88,25 +88,37 @@ __global__ void __launch_bounds__(kRouteThreads)
   if (e >= 0) pos[i] = wcnt[warp][e] + lrank;
 }
 
-__global__ void moe_route_scan_kernel(int nblocks, int E, int64_t row_bytes,
-                                      int32_t* __restrict__ blk, int64_t* __restrict__ counts,
-                                      int64_t* __restrict__ seg_rows,
-                                      int64_t* __restrict__ demand_row) {
+// one warp per expert column of blk: 32 block totals per round loaded in
+// parallel, warp exclusive scan + carry (no dependent global-load chain)
+constexpr int kScanThreads = 1024;
+__global__ void __launch_bounds__(kScanThreads)
+    moe_route_scan_kernel(int nblocks, int E, int64_t row_bytes, int32_t* __restrict__ blk,
+                          int64_t* __restrict__ counts, int64_t* __restrict__ seg_rows,
+                          int64_t* __restrict__ demand_row) {
   __shared__ int64_t s_cnt[kMaxExperts];
-  const int e = threadIdx.x;
-  if (e < E) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int e = warp; e < E; e += kScanThreads / 32) {
     int64_t run = 0;
-    for (int b = 0; b < nblocks; ++b) {
-      const int c = blk[(int64_t)b * E + e];
-      blk[(int64_t)b * E + e] = (int32_t)run;  // becomes the block base
-      run += c;
+    for (int b0 = 0; b0 < nblocks; b0 += 32) {
+      const int b = b0 + lane;
+      const int c = b < nblocks ? blk[(int64_t)b * E + e] : 0;
+      int x = c;  // inclusive warp scan
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+      }
+      if (b < nblocks) blk[(int64_t)b * E + e] = (int32_t)(run + x - c);  // block base
+      run += __shfl_sync(0xffffffffu, x, 31);
     }
-    s_cnt[e] = run;
-    counts[e] = run;
-    demand_row[e] = run * row_bytes;
+    if (lane == 0) {
+      s_cnt[e] = run;
+      counts[e] = run;
+      demand_row[e] = run * row_bytes;
+    }
   }
   __syncthreads();
-  if (e == 0) {
+  if (threadIdx.x == 0) {
     int64_t a = 0;
     for (int x = 0; x < E; ++x) {
       seg_rows[x] = a;
@@ -334,7 +346,7 @@ int fast_moe_route(const int32_t* topk, int T, int k, int E, int64_t row_bytes, 
   const int nb = N > 0 ? (N + kRouteThreads - 1) / kRouteThreads : 0;
   if (nb > 0)
     moe_route_local_kernel<<<nb, kRouteThreads, 0, s>>>(topk, N, E, pos, (int32_t*)workspace);
-  moe_route_scan_kernel<<<1, 64, 0, s>>>(nb, E, row_bytes, (int32_t*)workspace, counts,
+  moe_route_scan_kernel<<<1, kScanThreads, 0, s>>>(nb, E, row_bytes, (int32_t*)workspace, counts,
                                          seg_rows, demand_row);
   return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
 }
