@@ -48,16 +48,34 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > lib_m for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None,
+          out: str | None = None) -> str:
+    """Compile each translation unit in parallel (nvcc -c), then link the
+    shared library.  `extra` flags (e.g. -DFAST_EXEC_FUZZ) and `out` build a
+    variant library next to the product one."""
+    out = out or LIB_PATH
+    if not force and out == LIB_PATH and not needs_build():
         return LIB_PATH
-    cmd = [_nvcc(), *NVCC_FLAGS, f"-I{INCLUDE}", f"-I{CSRC}", "-o", LIB_PATH + ".tmp",
-           *sources()]
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
-    os.replace(LIB_PATH + ".tmp", LIB_PATH)
-    return LIB_PATH
+    nvcc = _nvcc()
+    objdir = os.path.join(PKG_DIR, "_obj", os.path.basename(out))
+    os.makedirs(objdir, exist_ok=True)
+    comp = [f for f in NVCC_FLAGS if f != "-shared"] + list(extra or [])
+    procs, objs = [], []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [nvcc, *comp, f"-I{INCLUDE}", f"-I{CSRC}", "-c", "-o", obj, src]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        procs.append(subprocess.Popen(cmd))
+        objs.append(obj)
+    bad = [p.args[-1] for p in procs if p.wait() != 0]
+    if bad:
+        raise RuntimeError(f"nvcc failed on {bad}")
+    link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "--cudart", "static",
+            "-o", out + ".tmp", *objs]
+    subprocess.run(link, check=True)
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

@@ -36,8 +36,14 @@ def partitions(world: int):
 def main() -> int:
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
-    dist.init_process_group("nccl")
+    # FAST_MP_ONE_GPU=1: every rank on cuda:0 (a 1-GPU box).  The data path is
+    # still the product one -- separate processes, CUDA-IPC mappings of each
+    # other's symmetric blocks, system-scope flags -- but NCCL refuses two
+    # ranks on one device, so the bootstrap is gloo and the all_to_all_single
+    # comparisons use the CPU oracle instead of NCCL.
+    one_gpu = os.environ.get("FAST_MP_ONE_GPU") == "1"
+    torch.cuda.set_device(0 if one_gpu else int(os.environ.get("LOCAL_RANK", rank)))
+    dist.init_process_group("gloo" if one_gpu else "nccl")
     ok = True
     for (n, m) in partitions(world):
         cases = [workloads.zipf_sizes(5, world, 1.2, 8_000_003),
@@ -65,15 +71,21 @@ def main() -> int:
         # all_to_all_fast vs NCCL all_to_all_single (rows of 4096 bf16)
         rng = np.random.default_rng(42)
         splits = rng.integers(0, 64, (world, world))
-        x = torch.randn(int(splits[rank].sum()), 4096, dtype=torch.bfloat16, device="cuda")
+        xs = [torch.randn(int(splits[g].sum()), 4096, dtype=torch.bfloat16,
+                          generator=torch.Generator().manual_seed(77 + g)) for g in range(world)]
+        x = xs[rank].cuda()
         out_rows = int(splits[:, rank].sum())
         y_fast = torch.empty(out_rows, 4096, dtype=torch.bfloat16, device="cuda")
-        y_nccl = torch.empty_like(y_fast)
         all_to_all_fast(y_fast, x, splits[:, rank].tolist(), splits[rank].tolist(), comm=comm)
-        dist.all_to_all_single(y_nccl, x, splits[:, rank].tolist(), splits[rank].tolist())
+        if one_gpu:  # all_to_all_single semantics on the host
+            y_ref = torch.cat([xs[g][int(splits[g, :rank].sum()):int(splits[g, :rank + 1].sum())]
+                               for g in range(world)])
+        else:
+            y_ref = torch.empty_like(y_fast)
+            dist.all_to_all_single(y_ref, x, splits[:, rank].tolist(), splits[rank].tolist())
         torch.cuda.synchronize()
         comm.check()
-        if not torch.equal(y_fast.view(torch.int16), y_nccl.view(torch.int16)):
+        if not torch.equal(y_fast.cpu().view(torch.int16), y_ref.cpu().view(torch.int16)):
             print(f"[rank {rank}] all_to_all_fast != all_to_all_single (n={n}, m={m})", flush=True)
             ok = False
         # MoE dispatch (config 3 shape, scaled): expert inputs vs the oracle
@@ -130,7 +142,7 @@ def main() -> int:
         mcomm.close()
         comm.close()
         dist.barrier()
-    flag = torch.tensor([0 if ok else 1], device="cuda")
+    flag = torch.tensor([0 if ok else 1], device="cpu" if one_gpu else "cuda")
     dist.all_reduce(flag)
     if rank == 0:
         print("MP_EXEC", "PASS" if int(flag.item()) == 0 else "FAIL", flush=True)
