@@ -42,6 +42,21 @@ typedef struct {
   int32_t to_gpu;
 } fast_move;
 
+/* Where the auxiliary padding of one NW-corner staircase cell (src, dst)
+ * runs out (strip_auxiliary, birkhoff.py:225-252: in decomposition order an
+ * edge pays its cell's remaining aux before real bytes).  `stage` is the raw
+ * index of the LAST stage that charged aux to the cell, `real` the real bytes
+ * that edge carried; raw stages before it that use the cell carry 0 real
+ * bytes, raw stages after it the full stage weight; every other edge carries
+ * the full weight.  stage = -1: unused slot.  With this table the per-edge
+ * stage_bytes [K][n] array (16.5 GB per config-5 batch) need not be written. */
+typedef struct {
+  int64_t real;
+  int32_t stage;
+  int16_t src;
+  int16_t dst;
+} fast_strip_rec;
+
 /* Packed schedules for a batch of B matrices with n servers x m GPUs,
  * G = n*m, T = n*(n-1) cross tiles, S = max(m-1,1) move slots per tile,
  * K = n*n-2n+2 stage capacity (birkhoff.py:188).  All device pointers.
@@ -59,11 +74,16 @@ typedef struct {
   int32_t *n_raw;       /* [B] raw (pre-strip) stage count */
   int64_t *stage_weight;/* [B][K] raw stage weights in decomposition order */
   uint8_t *stage_perm;  /* [B][K][n] dst server of src u in raw stage k */
-  int64_t *stage_bytes; /* [B][K][n] real bytes on edge (u, perm[u]) */
+  int64_t *stage_bytes; /* [B][K][n] real bytes on edge (u, perm[u]), or NULL
+                           (then use `strip`) */
   int32_t *n_stages;    /* [B] stages kept after stripping */
   int32_t *stage_order; /* [B][K] raw index of the k-th stage, ascending */
   int32_t *status;      /* [B] FAST_OK / FAST_EVALIDATION / FAST_EINVARIANT */
   void *workspace;      /* fast_synth_workspace_bytes(B, n) bytes */
+  /* optional outputs (NULL = not produced) */
+  fast_strip_rec *strip;/* [B][2n+2] aux run-out table (above) */
+  uint64_t *tile_mask;  /* [B][T] cells of each balanced cross tile that
+                           differ from D: bit p*m+q (m <= 8 only) */
 } fast_sched_bufs;
 
 /* Library / ABI version (major*10000 + minor*100 + patch). */
@@ -88,6 +108,18 @@ int fast_synth_batch(const int64_t *D, int B, int n, int m,
 int fast_synth_batch_ev(const int64_t *D, int B, int n, int m,
                         const fast_sched_bufs *out, void *stream,
                         void *const *events);
+
+/* Compact result for shipping a batch to the host (the e2e path): after
+ * fast_synth_batch with `tile_mask` set, gather the changed cells of every
+ * balanced cross tile (tile order i-major, then bit order) into `vals` and
+ * write val_base[b] = first value of matrix b (exclusive prefix, val_base[B]
+ * = total).  The host rebuilds `balanced` as D with those cells replaced
+ * (10.3 of 64 cells per tile at config 5: 1.5 MB instead of 8.4 MB per
+ * matrix).  vals capacity: B*T*m*m.  m <= 8. */
+size_t fast_compact_workspace_bytes(int B);
+int fast_compact_batch(const fast_sched_bufs *out, int B, int n, int m,
+                       int64_t *vals, int64_t *val_base, void *workspace,
+                       void *stream);
 
 /* build_balance_plan only (balance.py:139-174): fills balanced, server,
  * move_count, moves, status. */

@@ -36,7 +36,7 @@ class FastSchedBufs(ctypes.Structure):
     _fields_ = [(name, ctypes.c_void_p) for name in (
         "balanced", "server", "move_count", "moves", "common_sum", "aux",
         "n_raw", "stage_weight", "stage_perm", "stage_bytes", "n_stages",
-        "stage_order", "status", "workspace")]
+        "stage_order", "status", "workspace", "strip", "tile_mask")]
 
 
 class FastPlan(ctypes.Structure):
@@ -64,6 +64,10 @@ SIGNATURES: list[tuple[str, object, list]] = [
     ("fast_decompose_batch", ctypes.c_int,
      [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
       ctypes.POINTER(FastSchedBufs), ctypes.c_void_p]),
+    ("fast_compact_workspace_bytes", ctypes.c_size_t, [ctypes.c_int]),
+    ("fast_compact_batch", ctypes.c_int,
+     [ctypes.POINTER(FastSchedBufs), ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
 ]
 
 _lib: ctypes.CDLL | None = None

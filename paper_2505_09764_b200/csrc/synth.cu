@@ -154,7 +154,9 @@ __global__ void __launch_bounds__(kBalThreads)
       const int slots = m > 1 ? m - 1 : 1;
       const int tidx = i * (n - 1) + (j < i ? j : j - 1);
       fast_move* mv = out.moves + ((int64_t)b * T + tidx) * slots;
-      int nm = balance_tile<M>(t, m, mv, slots, M ? rs : nullptr);
+      uint64_t mk = 0;
+      int nm = balance_tile<M>(t, m, mv, slots, M ? rs : nullptr, &mk);
+      if (out.tile_mask) out.tile_mask[(int64_t)b * T + tidx] = mk;
       if (nm < 0) {
         raise_status(st, FAST_EINVARIANT);
         nm = 0;
@@ -237,6 +239,93 @@ __global__ void __launch_bounds__(1024)
   }
   int32_t* ord = out.stage_order + (int64_t)b * K;
   for (int i = threadIdx.x; i < kept; i += blockDim.x) ord[i] = (int32_t)(kt[i] & 0xffffu);
+}
+
+// ---------------------------------------------------------------------------
+// Compact result (fast_compact_batch): the changed cells of the balanced
+// cross tiles, gathered per matrix in tile order then bit order.
+__device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* sh_warp, int64_t& total) {
+  // blockDim.x == kCompactThreads; sh_warp holds one slot per warp
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh_warp[warp] = x;
+  __syncthreads();
+  int64_t wbase = 0, tot = 0;
+  for (int w = 0; w < nw; ++w) {
+    const int64_t t = sh_warp[w];
+    if (w < warp) wbase += t;
+    tot += t;
+  }
+  __syncthreads();
+  total = tot;
+  return wbase + x - v;
+}
+
+constexpr int kCompactThreads = 512;
+
+__global__ void __launch_bounds__(kCompactThreads)
+    compact_count_kernel(const fast_sched_bufs out, const int T, int64_t* __restrict__ cnt) {
+  __shared__ int64_t shw[kCompactThreads / 32];
+  const int b = blockIdx.x;
+  int64_t c = 0;
+  if (out.status[b] == FAST_OK)
+    for (int t = threadIdx.x; t < T; t += blockDim.x)
+      c += __popcll(out.tile_mask[(int64_t)b * T + t]);
+  int64_t tot;
+  block_excl_scan(c, shw, tot);
+  if (threadIdx.x == 0) cnt[b] = tot;
+}
+
+__global__ void __launch_bounds__(kCompactThreads)
+    compact_scan_kernel(const int64_t* __restrict__ cnt, const int B, int64_t* __restrict__ base) {
+  __shared__ int64_t shw[kCompactThreads / 32];
+  int64_t carry = 0;
+  for (int b0 = 0; b0 < B; b0 += blockDim.x) {
+    const int i = b0 + threadIdx.x;
+    const int64_t v = i < B ? cnt[i] : 0;
+    int64_t tot;
+    const int64_t ex = block_excl_scan(v, shw, tot);
+    if (i < B) base[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) base[B] = carry;
+}
+
+// one CTA per matrix; rounds of blockDim consecutive tiles (coalesced mask
+// reads), a block scan places each tile's values
+__global__ void __launch_bounds__(kCompactThreads)
+    compact_pack_kernel(const fast_sched_bufs out, const int n, const int m,
+                        const int64_t* __restrict__ base, int64_t* __restrict__ vals) {
+  __shared__ int64_t shw[kCompactThreads / 32];
+  const int b = blockIdx.x;
+  if (out.status[b] != FAST_OK) return;
+  const int T = n * (n - 1);
+  const int64_t G = (int64_t)n * m;
+  const uint64_t* mk = out.tile_mask + (int64_t)b * T;
+  const int64_t* Bb = out.balanced + (int64_t)b * G * G;
+  int64_t o = base[b];
+  for (int t0 = 0; t0 < T; t0 += blockDim.x) {
+    const int t = t0 + threadIdx.x;
+    uint64_t x = t < T ? mk[t] : 0ull;
+    int64_t tot;
+    int64_t w = o + block_excl_scan(__popcll(x), shw, tot);
+    if (x) {
+      const int i = t / (n - 1), jj = t - i * (n - 1), j = jj < i ? jj : jj + 1;
+      const int64_t* tile = Bb + (int64_t)i * m * G + (int64_t)j * m;
+      while (x) {
+        const int bit = __ffsll((long long)x) - 1;
+        x &= x - 1;
+        const int p = bit / m, q = bit - p * m;
+        vals[w++] = tile[(int64_t)p * G + q];
+      }
+    }
+    o += tot;
+  }
 }
 
 size_t sort_smem_bytes(int n) {
@@ -354,11 +443,28 @@ int fast_debug_dec_prof(unsigned long long* out8, int reset) {
 }
 #endif
 
-int fast_version(void) { return 100; }
+int fast_version(void) { return 200; }
 
 size_t fast_synth_workspace_bytes(int B, int n) {
   if (B <= 0 || n < 2 || n > FAST_MAX_SERVERS) return 0;
   return (size_t)B * dec_ws_bytes_per_matrix(n);
+}
+
+size_t fast_compact_workspace_bytes(int B) { return (size_t)(B > 0 ? B : 1) * 8 + 256; }
+
+int fast_compact_batch(const fast_sched_bufs* out, int B, int n, int m, int64_t* vals,
+                       int64_t* val_base, void* workspace, void* stream) {
+  if (bad_shape(B, n, m) || !out || !out->tile_mask || !out->balanced || m > 8 || !val_base ||
+      !workspace)
+    return FAST_EVALIDATION;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (B == 0) return check(cudaMemsetAsync(val_base, 0, 8, s));
+  int64_t* cnt = (int64_t*)workspace;
+  const int T = n * (n - 1);
+  compact_count_kernel<<<B, kCompactThreads, 0, s>>>(*out, T, cnt);
+  compact_scan_kernel<<<1, kCompactThreads, 0, s>>>(cnt, B, val_base);
+  if (vals) compact_pack_kernel<<<B, kCompactThreads, 0, s>>>(*out, n, m, val_base, vals);
+  return check(cudaGetLastError());
 }
 
 int fast_balance_batch(const int64_t* D, int B, int n, int m,

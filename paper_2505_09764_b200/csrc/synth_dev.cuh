@@ -37,7 +37,8 @@ __host__ __device__ __forceinline__ int stage_cap(int n) {
 template <int M>
 __device__ int balance_tile(int64_t* __restrict__ t, const int m_rt,
                             fast_move* __restrict__ out, const int slots,
-                            const int64_t* rowsum = nullptr) {
+                            const int64_t* rowsum = nullptr,
+                            uint64_t* changed = nullptr) {
   constexpr int MM = M ? M : FAST_MAX_GPUS_PER_SERVER;
   const int m = M ? M : m_rt;
   int64_t dev[MM];
@@ -61,6 +62,9 @@ __device__ int balance_tile(int64_t* __restrict__ t, const int m_rt,
     if (p < m) dev[p] -= base + (p < extra ? 1 : 0);
 
   int nmoves = 0;
+  // cells touched by a transfer (m <= 8): shedding rows only lose and
+  // receiving rows only gain bytes, so touched == changed
+  uint64_t mk = 0;
   for (;;) {
     // over[0]: largest positive deviation, lowest index on ties;
     // under[0]: most negative deviation, lowest index on ties.
@@ -74,7 +78,10 @@ __device__ int balance_tile(int64_t* __restrict__ t, const int m_rt,
         if (d < dh) { dh = d; h = p; }
       }
     }
-    if (g < 0) return nmoves;
+    if (g < 0) {
+      if (changed) *changed = mk;
+      return nmoves;
+    }
     if (h < 0 || nmoves >= slots) return -1;
     const int64_t chunk = dg < -dh ? dg : -dh;
     int64_t left = chunk;
@@ -93,6 +100,7 @@ __device__ int balance_tile(int64_t* __restrict__ t, const int m_rt,
       rg[q] -= take;
       rh[q] += take;
       left -= take;
+      if (m <= 8) mk |= (1ull << (g * m + q)) | (1ull << (h * m + q));
     }
 #pragma unroll
     for (int p = 0; p < MM; ++p) {
@@ -633,6 +641,9 @@ __device__ __forceinline__ void decompose_one(char* wsm, const int64_t* __restri
     }
     if (NWP > NW && lane == 0) s.sup[u * NWP + ((NWP - 1) ^ 1)] = 0u;
   }
+  fast_strip_rec* const strip = out.strip ? out.strip + (int64_t)b * (2 * n + 2) : nullptr;
+  if (strip)
+    for (int c = lane; c < 2 * n + 2; c += 32) strip[c].stage = -1;
   if (lane == 0) {
     out.common_sum[b] = common;
     // NW-corner staircase: row u's aux cells are the contiguous columns whose
@@ -707,7 +718,7 @@ __device__ __forceinline__ void decompose_one(char* wsm, const int64_t* __restri
   int k = 0, kept = 0;
   int64_t* wout = out.stage_weight + (int64_t)b * K;
   uint8_t* pout = out.stage_perm + (int64_t)b * K * n;
-  int64_t* bout = out.stage_bytes + (int64_t)b * K * n;
+  int64_t* bout = out.stage_bytes ? out.stage_bytes + (int64_t)b * K * n : nullptr;
   while (remaining > 0) {
     DPROF_T(t0);
     if (k >= K) { st = FAST_EINVARIANT; break; }
@@ -728,11 +739,20 @@ __device__ __forceinline__ void decompose_one(char* wsm, const int64_t* __restri
       // strip_auxiliary (birkhoff.py:225-252): the cell pays aux first
       const int64_t charged = am[r] < weight ? am[r] : weight;
       const int64_t real = weight - charged;
+      const bool last_aux = charged > 0 && charged == am[r];  // the cell's aux runs out
       am[r] -= charged;
       mv[r] -= weight;
       if (valid) {
-        __stcs(bout + (int64_t)k * n + u, real);
+        if (bout) __stcs(bout + (int64_t)k * n + u, real);
         pout[(int64_t)k * n + u] = (uint8_t)v;
+        if (strip && last_aux) {
+          fast_strip_rec rec;
+          rec.real = real;
+          rec.stage = k;
+          rec.src = (int16_t)u;
+          rec.dst = (int16_t)v;
+          strip[abase[r] + v] = rec;
+        }
       }
       const uint32_t rb = __ballot_sync(0xffffffffu, valid && real > 0);
       const uint32_t zb = __ballot_sync(0xffffffffu, valid && mv[r] == 0);
