@@ -27,6 +27,8 @@ import sys
 import tempfile
 import time
 
+import numpy as np
+
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
@@ -101,27 +103,73 @@ def synth_inputs(args, device):
 
 
 def algorithmic_bytes_decompose(n: int, n_raw) -> int:
-    # read server matrix, write aux, write each raw stage (weight + perm + bytes)
-    return int(sum(16 * n * n + int(k) * (8 + 9 * n) for k in n_raw))
+    # read server matrix, write aux, write each raw stage (weight + perm)
+    return int(sum(16 * n * n + int(k) * (8 + n) for k in n_raw))
+
+
+# Dependent-chain floor of one DFS step of the decomposition (cycles):
+# ld.shared.v4 (34.6) -> and -> bfind (~16) -> mad -> 2 x selp -> next load,
+# measured with tools/op_lat.cu / tools/chase2_micro.cu (profiles/README.md).
+DFS_STEP_FLOOR_CYCLES = 70.0
+
+SUBSET_KEYS = ("balanced", "server", "move_count", "moves", "common_sum", "aux", "n_raw",
+               "stage_weight", "stage_perm", "n_stages", "stage_order", "status", "strip")
+
+
+def device_subset(bufs, k: int) -> dict:
+    """Host copy of the first k matrices of a SynthBuffers (parity check)."""
+    return {key: getattr(bufs, key)[:k].cpu().numpy() for key in SUBSET_KEYS}
+
+
+def compare_with_oracle(ref: dict, b: int, got: dict, what: str) -> None:
+    """Bit-exact comparison of one matrix's schedule with the oracle's."""
+    from paper_2505_09764_b200.schedule import MOVE_DTYPE
+
+    k, s = int(ref["n_raw"][b]), int(ref["n_stages"][b])
+    checks = [("status", got["status"] == ref["status"][b]),
+              ("balanced", np.array_equal(got["balanced"], ref["balanced"][b])),
+              ("server", np.array_equal(got["server"], ref["server"][b])),
+              ("move_count", np.array_equal(got["move_count"], ref["move_count"][b])),
+              ("common_sum", got["common_sum"] == ref["common_sum"][b]),
+              ("aux", np.array_equal(got["aux"], ref["aux"][b])),
+              ("n_raw", got["n_raw"] == k), ("n_stages", got["n_stages"] == s),
+              ("stage_weight", np.array_equal(got["stage_weight"][:k], ref["stage_weight"][b, :k])),
+              ("stage_perm", np.array_equal(got["stage_perm"][:k], ref["stage_perm"][b, :k])),
+              ("stage_bytes", np.array_equal(got["stage_bytes"][:k], ref["stage_bytes"][b, :k])),
+              ("stage_order", np.array_equal(got["stage_order"][:s], ref["stage_order"][b, :s]))]
+    mv = got["moves"].view(MOVE_DTYPE).reshape(ref["moves"].shape[1:])
+    cnt = ref["move_count"][b]
+    used = np.arange(mv.shape[1])[None, :] < cnt[:, None]
+    checks.append(("moves", np.array_equal(mv[used], ref["moves"][b][used])))
+    bad = [name for name, ok in checks if not bool(ok)]
+    if bad:
+        raise RuntimeError(f"PARITY FAILURE ({what}, matrix {b}): {bad}")
 
 
 def bench_synth(args) -> dict:
     import torch
 
     from paper_2505_09764_b200 import _lib, synth
+    from paper_2505_09764_b200.schedule import STRIP_DTYPE, stage_bytes_from_strip
 
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     lib = _lib.load()
     n, m, B = args.n, args.m, args.batch
-    G = n * m
+    G, T = n * m, n * (n - 1)
     D = synth_inputs(args, dev)
-    bufs = synth.SynthBuffers(B, n, m, dev)
+    # the batch product layout: no per-edge stage_bytes (the strip table
+    # replaces it), changed-cell masks + the compact pack of the balanced tiles
+    bufs = synth.SynthBuffers(B, n, m, dev, stage_bytes=False, compact=True)
+    vals = torch.empty(B * T * m * m, dtype=torch.int64, device=dev)
+    vbase = torch.empty(B + 1, dtype=torch.int64, device=dev)
+    cws = torch.empty(int(lib.fast_compact_workspace_bytes(B)), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
     sh = ctypes.c_void_p(stream.cuda_stream)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
 
     def make_events(k):
-        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(k)]
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(k)]
         for row in evs:
             for e in row:
                 e.record(stream)  # materialise the handles
@@ -130,10 +178,14 @@ def bench_synth(args) -> dict:
     def step(ev_row=None):
         arr = None
         if ev_row is not None:
-            arr = (ctypes.c_void_p * 4)(*[e.cuda_event for e in ev_row])
-        rc = lib.fast_synth_batch_ev(ctypes.c_void_p(D.data_ptr()), B, n, m,
-                                     ctypes.byref(bufs.struct), sh, arr)
+            arr = (ctypes.c_void_p * 4)(*[e.cuda_event for e in ev_row[:4]])
+        rc = lib.fast_synth_batch_ev(P(D), B, n, m, ctypes.byref(bufs.struct), sh, arr)
         _lib.check_rc(rc, "fast_synth_batch_ev")
+        rc = lib.fast_compact_batch(ctypes.byref(bufs.struct), B, n, m, P(vals), P(vbase), P(cws),
+                                    sh)
+        _lib.check_rc(rc, "fast_compact_batch")
+        if ev_row is not None:
+            ev_row[4].record(stream)
 
     for _ in range(args.warmup):
         step()
@@ -152,14 +204,21 @@ def bench_synth(args) -> dict:
         t1.record(stream)
         torch.cuda.synchronize()
     total_ms = t0.elapsed_time(t1)
-    per = {"balance_kernel": 0.0, "decompose_kernel": 0.0, "sort_kernel": 0.0}
+    names = ("balance_kernel", "decompose_kernel", "sort_kernel", "compact_kernels")
+    per = {k: 0.0 for k in names}
     for row in evs:
-        per["balance_kernel"] += row[0].elapsed_time(row[1])
-        per["decompose_kernel"] += row[1].elapsed_time(row[2])
-        per["sort_kernel"] += row[2].elapsed_time(row[3])
+        for i, k in enumerate(names):
+            per[k] += row[i].elapsed_time(row[i + 1])
     per = {k: v / args.steps for k, v in per.items()}
     ms_step = total_ms / args.steps
     n_raw = bufs.n_raw.cpu().tolist()
+    P_CHECK = min(64, B)
+    dev_sub = device_subset(bufs, P_CHECK)
+    dev_sub["stage_bytes"] = [stage_bytes_from_strip(dev_sub["stage_weight"][b, :n_raw[b]],
+                                                     dev_sub["stage_perm"][b, :n_raw[b]],
+                                                     dev_sub["strip"][b].view(STRIP_DTYPE).reshape(-1))
+                              for b in range(P_CHECK)]
+    d2h_device_layout = int(bufs.output_nbytes())
 
     peaks, peak_kind = measured_peaks()
     hbm = float(peaks["hbm_gbs"])
@@ -179,26 +238,27 @@ def bench_synth(args) -> dict:
                 "kernel_ms": {k: round(v, 4) for k, v in per.items()},
                 "balance_kernel_gbs": round(alg["balance_kernel"] / (per["balance_kernel"] * 1e-3) / 1e9, 1),
                 "balance_kernel_frac": round(alg["balance_kernel"] / (per["balance_kernel"] * 1e-3) / 1e9 / hbm, 4),
-                "note": "decompose is a dependent chain of <= n^2-2n+2 peels per matrix "
-                        "(latency-bound: one Kuhn re-augmentation of ~n/2 dependent "
-                        "shared-memory steps per peel); balance is the HBM-bound kernel"}
+                "note": "decompose is a dependent chain (see `chain`); its HBM fraction is "
+                        "reported for completeness only. balance is the HBM-bound kernel"}
     sm_hz = None
     try:
         sm_hz = torch.cuda.get_device_properties(0).clock_rate * 1e3
     except Exception:
         pass
-    if sm_hz:
-        peels = sum(n_raw) / len(n_raw)
-        roofline["decompose_cycles_per_peel"] = round(per["decompose_kernel"] * 1e-3 * sm_hz / peels, 1)
+    if not sm_hz:
+        sm_hz = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    peels = sum(n_raw) / len(n_raw)
+    roofline["decompose_cycles_per_peel"] = round(per["decompose_kernel"] * 1e-3 * sm_hz / peels, 1)
 
-    # ---- e2e: host (pinned) D -> device -> synth -> packed schedule -> host,
+    # ---- e2e: host (pinned) D -> device -> synth -> compact result -> host,
     # through synthesize_host_batch (chunked, copies overlapped with kernels)
     e2e = None
+    hs = Dh = None
     if not args.no_e2e:
         Dh = torch.empty(D.shape, dtype=D.dtype, pin_memory=True)
         Dh.copy_(D)
         hs = synth.HostSchedules(B, n, m)
-        del bufs
+        del bufs, vals
         torch.cuda.empty_cache()
         synth.synthesize_host_batch(Dh, n, m, hs, chunk=args.e2e_chunk)  # warm-up
         steps = max(1, min(args.steps, 3))
@@ -212,16 +272,44 @@ def bench_synth(args) -> dict:
         e2e = {"value": round(B / (ems * 1e-3), 3), "unit": "matrices/s",
                "h2d_bytes_per_step": int(Dh.numel() * 8), "d2h_bytes_per_step": int(hs.nbytes()),
                "ms_per_step": round(ems, 3), "steps": steps,
-               "path": f"synthesize_host_batch (C-ABI fast_synth_batch per {args.e2e_chunk}-matrix "
-                       "chunk, pinned host buffers, H2D/kernels/D2H overlapped; wall clock "
-                       "incl. the final host sync)"}
-        del Dh, hs
+               "d2h_full_device_layout_bytes": d2h_device_layout,
+               "path": f"synthesize_host_batch (C-ABI fast_synth_batch + fast_compact_batch per "
+                       f"{args.e2e_chunk}-matrix chunk, pinned host D in, compact schedule out "
+                       "(HostSchedules: moves, stages, aux run-out table, changed cells of the "
+                       "balanced tiles); H2D/kernels/D2H overlapped; wall clock incl. the final "
+                       "host sync)"}
 
-    cpu = None
+    cpu, parity = None, None
     if not args.no_cpu_baseline:
-        cpu = cpu_baseline_synth(args, D)
+        cpu, ref = cpu_baseline_synth(args, D)
+        k_chk = min(P_CHECK, int(ref["n_raw"].shape[0]))
+        for b in range(k_chk):
+            got = {key: dev_sub[key][b] for key in SUBSET_KEYS}
+            got["stage_bytes"] = dev_sub["stage_bytes"][b]
+            compare_with_oracle(ref, b, got, "device path")
+            if hs is not None:
+                p = hs.packed(b, Dh[b].numpy())
+                compare_with_oracle(ref, b, dict(
+                    status=p.status, balanced=p.balanced, server=p.server,
+                    move_count=p.move_count, moves=p.moves.view(np.int64).reshape(-1, 2),
+                    common_sum=p.common_sum, aux=p.aux, n_raw=p.n_raw, n_stages=p.n_stages,
+                    stage_weight=p.stage_weight, stage_perm=p.stage_perm,
+                    stage_bytes=p.stage_bytes, stage_order=p.stage_order), b, "e2e compact path")
+        steps_mean = cpu.pop("_dfs_steps_mean")
+        parity = {"parity_checked": k_chk, "against": "oracle/fast_oracle.c (pinned to tiersched "
+                  "by tests/golden/headline_digests.json)", "paths": ["device", "e2e"] if hs is not None
+                  else ["device"], "result": "bit-exact"}
+        cyc = per["decompose_kernel"] * 1e-3 * sm_hz / steps_mean
+        roofline["chain"] = {
+            "bound": "dependent shared-memory chain (Kuhn DFS)", "kernel": "decompose_kernel",
+            "dfs_steps_per_matrix": round(steps_mean, 1),
+            "steps_source": f"oracle DFS step counter on the {k_chk} checked matrices",
+            "cycles_per_step": round(cyc, 1), "floor_cycles_per_step": DFS_STEP_FLOOR_CYCLES,
+            "frac": round(DFS_STEP_FLOOR_CYCLES / cyc, 4),
+            "note": "whole-kernel cycles (all chains resident, kernel time = slowest chain) per DFS "
+                    "step; the floor is one step's dependent LDS->and->bfind->mad->selp chain"}
 
-    return {
+    out = {
         "metric": "schedule synthesis throughput (FAST synthesize_fast, batch of 1000 traffic "
                   "matrices, config 5)",
         "value": round(B / (ms_step * 1e-3), 3), "unit": "matrices/s",
@@ -230,32 +318,76 @@ def bench_synth(args) -> dict:
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
         "data": "synthetic (Zipf 0.8 traffic matrices, seeds 0..B-1, generated on device)",
         "config": {"workload": "config5_synthesis", "n_servers": n, "gpus_per_server": m,
-                   "batch": B, "zipf_skew": args.skew, "total_bytes": args.total,
-                   "l2": "inputs larger than L2 (D batch = %.1f GB)" % (B * G * G * 8 / 1e9)
-                   if B * G * G * 8 > 126e6 else "inputs within L2"},
+                   "batch": B, "zipf_skew": args.skew, "total_bytes": args.total},
+        "l2": "inputs larger than L2 (D batch = %.1f GB)" % (B * G * G * 8 / 1e9)
+              if B * G * G * 8 > 126e6 else "inputs within L2",
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": 3 * args.steps, "clocks": clk.summary(),
-        "stages_per_matrix_mean": round(sum(n_raw) / len(n_raw), 1),
+        "gpu_launches": 6 * args.steps, "clocks": clk.summary(),
+        "stages_per_matrix_mean": round(peels, 1),
     }
+    if parity is not None:
+        out["parity"] = parity
+        out["parity_checked"] = parity["parity_checked"]
+    if not args.no_latency:
+        out["latency"] = single_matrix_latency(args)
+    return out
 
 
-def cpu_baseline_synth(args, D, budget_s: float = 12.0) -> dict:
-    """C oracle port (single thread) on a bounded sample of the same batch."""
+def single_matrix_latency(args) -> dict:
+    """Per-matrix synthesis LATENCY at 1 GPU (one matrix per call, B = 1),
+    n = 16..128 x 8, Zipf 0.8: device time of fast_synth_batch from CUDA
+    events, median of a few calls."""
+    import torch
+
+    from paper_2505_09764_b200 import _lib, synth, workloads
+
+    lib = _lib.load()
+    stream = torch.cuda.current_stream()
+    sh = ctypes.c_void_p(stream.cuda_stream)
+    res = {}
+    for n in (16, 32, 64, 128):
+        G = n * args.m
+        D = workloads.zipf_batch_device([0], G, args.skew, args.total, torch.device("cuda", 0))
+        bufs = synth.SynthBuffers(1, n, args.m, D.device, stage_bytes=False, compact=True)
+        times = []
+        reps = 5 if n < 128 else 3
+        for r in range(reps + 1):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            _lib.check_rc(lib.fast_synth_batch(ctypes.c_void_p(D.data_ptr()), 1, n, args.m,
+                                               ctypes.byref(bufs.struct), sh), "fast_synth_batch")
+            b.record(stream)
+            b.synchronize()
+            if r:
+                times.append(a.elapsed_time(b))
+        res[f"n{n}"] = {"us": round(statistics.median(times) * 1e3, 1),
+                        "stages": int(bufs.n_raw.item())}
+    return {"what": "one matrix per call (B=1), device time, median", "unit": "us", **res}
+
+
+def cpu_baseline_synth(args, D, budget_s: float = 12.0) -> tuple[dict, dict]:
+    """C oracle port (single thread) on a bounded sample of the same batch.
+    Returns the baseline line and the oracle's results (the parity check of
+    the timed batch)."""
     from oracle import oracle
 
     n, m = args.n, args.m
     Dh = D[: min(64, D.shape[0])].cpu().numpy()
     oracle.synthesize_batch(Dh[:1], n, m)  # load / warm
-    done, t0 = 0, time.perf_counter()
+    oracle.dfs_counters(reset=True)
+    done, t0, outs = 0, time.perf_counter(), []
     while done < Dh.shape[0]:
-        oracle.synthesize_batch(Dh[done:done + 1], n, m)
+        outs.append(oracle.synthesize_batch(Dh[done:done + 1], n, m))
         done += 1
         if time.perf_counter() - t0 > budget_s:
             break
     el = time.perf_counter() - t0
-    return {"value": round(done / el, 4), "unit": "matrices/s", "cores": 1, "kind": "port",
-            "sample": f"{done} matrices of the benchmark batch (n={n}, m={m}), "
-                      f"C restatement oracle/fast_oracle.c, 1 thread, {el:.1f} s"}
+    steps, _ = oracle.dfs_counters(reset=True)
+    ref = {k: np.concatenate([o[k] for o in outs]) for k in outs[0]}
+    return ({"value": round(done / el, 4), "unit": "matrices/s", "cores": 1, "kind": "port",
+             "sample": f"{done} matrices of the benchmark batch (n={n}, m={m}), "
+                       f"C restatement oracle/fast_oracle.c, 1 thread, {el:.1f} s",
+             "_dfs_steps_mean": steps / done}, ref)
 
 
 # ---------------------------------------------------------------------------
@@ -359,6 +491,7 @@ def main() -> None:
     ap.add_argument("--hidden", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--e2e-chunk", type=int, default=125)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup

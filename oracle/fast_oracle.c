@@ -217,11 +217,24 @@ typedef struct {
     unsigned char *seen;
 } fo_dec;
 
+/* DFS work counters (measurement only: bench.py reports the GPU kernel's
+ * cycles per DFS step against them).  One step = one column newly marked
+ * seen, i.e. one iteration of the GPU search loop. */
+static int64_t fo_steps, fo_searches;
+int64_t fo_dfs_counters(int64_t *searches, int reset)
+{
+    int64_t s = fo_steps;
+    if (searches) *searches = fo_searches;
+    if (reset) fo_steps = fo_searches = 0;
+    return s;
+}
+
 static int fo_augment(fo_dec *d, int u) /* birkhoff.py:172-180 */
 {
     for (int v = 0; v < d->n; v++) {
         if (d->work[u * d->n + v] > 0 && !d->seen[v]) {
             d->seen[v] = 1;
+            fo_steps++;
             if (d->col_match[v] < 0 || fo_augment(d, d->col_match[v])) {
                 d->col_match[v] = u;
                 d->row_match[u] = v;
@@ -279,6 +292,7 @@ int fo_decompose_server(int n, const int64_t *S, int64_t *common_out,
 
     for (int u = 0; u < n && st == FO_OK; u++) {
         memset(d.seen, 0, n);
+        fo_searches++;
         if (!fo_augment(&d, u)) st = FO_EINVARIANT;
     }
     int64_t remaining = common;
@@ -315,6 +329,7 @@ int fo_decompose_server(int n, const int64_t *S, int64_t *common_out,
             int u = freed[f];
             if (d.row_match[u] < 0) {
                 memset(d.seen, 0, n);
+                fo_searches++;
                 if (!fo_augment(&d, u)) st = FO_EINVARIANT;
             }
         }

@@ -77,6 +77,16 @@ def synthesize_batch(D: np.ndarray, n: int, m: int) -> dict:
     return out
 
 
+def dfs_counters(reset: bool = True) -> tuple[int, int]:
+    """(DFS steps, searches) accumulated by the oracle since the last reset
+    (one step = one column newly marked seen in the Kuhn search)."""
+    lib = _load()
+    lib.fo_dfs_counters.restype = ctypes.c_int64
+    s = ctypes.c_int64()
+    steps = lib.fo_dfs_counters(ctypes.byref(s), ctypes.c_int(1 if reset else 0))
+    return int(steps), int(s.value)
+
+
 def decompose_server(S: np.ndarray) -> dict:
     """Oracle decompose_server_matrix + strip + sort for one n x n matrix."""
     S = np.ascontiguousarray(S, dtype=np.int64)

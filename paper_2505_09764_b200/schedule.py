@@ -18,6 +18,47 @@ from .model import DemandMatrix, ServerMatrix, ValidationError
 
 # numpy view of ``fast_move`` (include/fastb200.h)
 MOVE_DTYPE = np.dtype([("bytes", "<i8"), ("from_gpu", "<i4"), ("to_gpu", "<i4")])
+# numpy view of ``fast_strip_rec``
+STRIP_DTYPE = np.dtype([("real", "<i8"), ("stage", "<i4"), ("src", "<i2"), ("dst", "<i2")])
+
+
+def stage_bytes_from_strip(weight: np.ndarray, perm: np.ndarray, strip: np.ndarray) -> np.ndarray:
+    """Per-edge real bytes [k_raw, n] of the raw stages from the aux run-out
+    table (fast_strip_rec): strip_auxiliary (birkhoff.py:225-252) charges a
+    cell's aux before its real bytes, so every stage using an aux cell before
+    the record's stage carries 0 real bytes, that stage carries `real`, and
+    every other edge carries the full stage weight."""
+    weight = np.asarray(weight, dtype=np.int64)
+    sb = np.repeat(weight[:, None], perm.shape[1], axis=1)
+    for rec in strip[strip["stage"] >= 0]:
+        u, v, kl = int(rec["src"]), int(rec["dst"]), int(rec["stage"])
+        ks = np.flatnonzero(perm[:kl, u] == v)
+        sb[ks, u] = 0
+        sb[kl, u] = int(rec["real"])
+    return sb
+
+
+def balanced_from_compact(D: np.ndarray, mask: np.ndarray, vals: np.ndarray, n: int,
+                          m: int) -> np.ndarray:
+    """Rebuild the balanced matrix from D and the compact cross-tile deltas
+    (fast_compact_batch): bit p*m+q of mask[t] marks a changed cell of cross
+    tile t (i-major order, j != i), vals holds their values in tile order
+    then bit order."""
+    bal = np.array(D, dtype=np.int64, copy=True)
+    T = n * (n - 1)
+    if T == 0:
+        return bal
+    bits = np.unpackbits(np.ascontiguousarray(mask).view(np.uint8).reshape(T, 8), axis=1,
+                         bitorder="little")[:, : m * m]
+    t_idx, bit = np.nonzero(bits)
+    if len(vals) != len(t_idx):
+        raise ValueError(f"compact result has {len(vals)} values for {len(t_idx)} changed cells")
+    i = t_idx // (n - 1)
+    jj = t_idx - i * (n - 1)
+    j = jj + (jj >= i)
+    p, q = bit // m, bit - (bit // m) * m
+    bal[i * m + p, j * m + q] = vals
+    return bal
 
 
 @dataclass(frozen=True)

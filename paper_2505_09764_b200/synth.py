@@ -28,8 +28,9 @@ import torch
 from . import _lib
 from .model import (DemandMatrix, InternalInvariantError, ServerMatrix, TileView, Topology,
                     ValidationError)
-from .schedule import (MOVE_DTYPE, BalancePlan, Decomposition, IntraMove, PackedSchedule,
-                       PermutationStage, Schedule, _fast_stage)
+from .schedule import (MOVE_DTYPE, STRIP_DTYPE, BalancePlan, Decomposition, IntraMove,
+                       PackedSchedule, PermutationStage, Schedule, _fast_stage,
+                       balanced_from_compact, stage_bytes_from_strip)
 
 FAST_MAX_SERVERS = 128  # include/fastb200.h
 
@@ -50,10 +51,15 @@ def _stream_handle(stream: torch.cuda.Stream | None) -> ctypes.c_void_p:
 
 
 class SynthBuffers:
-    """Device-resident packed schedules for a batch (fast_sched_bufs)."""
+    """Device-resident packed schedules for a batch (fast_sched_bufs).
+
+    stage_bytes=False skips the per-edge [B, K, n] real-byte array (the
+    decomposition then only records the aux run-out table, `strip`, from which
+    the host rebuilds it); compact=True adds the strip table and the changed-
+    cell masks of the balanced cross tiles (fast_compact_batch input)."""
 
     def __init__(self, B: int, n: int, m: int, device: torch.device | None = None,
-                 with_balance: bool = True):
+                 with_balance: bool = True, stage_bytes: bool = True, compact: bool = False):
         dev = device or _device()
         G, T, S, K = n * m, n * (n - 1), max(m - 1, 1), stage_cap(n)
         self.B, self.n, self.m = B, n, m
@@ -69,16 +75,20 @@ class SynthBuffers:
         self.n_raw = e(B, dt=i32)
         self.stage_weight = e(B, K, dt=i64)
         self.stage_perm = e(B, K, n, dt=u8)
-        self.stage_bytes = e(B, K, n, dt=i64)
+        self.stage_bytes = e(B, K, n, dt=i64) if stage_bytes or not compact else None
         self.n_stages = e(B, dt=i32)
         self.stage_order = e(B, K, dt=i32)
         self.status = e(B, dt=i32)
         ws = _lib.load().fast_synth_workspace_bytes(B, n)
         self.workspace = e(max(int(ws), 16), dt=u8)
-        self._struct = _lib.FastSchedBufs(*(t.data_ptr() for t in (
+        self.strip = e(B, 2 * n + 2, 2, dt=i64) if compact else None  # fast_strip_rec: 16 B
+        self.tile_mask = e(B, max(T, 1), dt=i64) if compact and m <= 8 else None
+        ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+        self._struct = _lib.FastSchedBufs(*(ptr(t) for t in (
             self.balanced, self.server, self.move_count, self.moves, self.common_sum,
             self.aux, self.n_raw, self.stage_weight, self.stage_perm, self.stage_bytes,
-            self.n_stages, self.stage_order, self.status, self.workspace)))
+            self.n_stages, self.stage_order, self.status, self.workspace, self.strip,
+            self.tile_mask)))
 
     @property
     def struct(self) -> _lib.FastSchedBufs:
@@ -89,24 +99,31 @@ class SynthBuffers:
         ts = (self.balanced, self.server, self.move_count, self.moves, self.common_sum,
               self.aux, self.n_raw, self.stage_weight, self.stage_perm, self.stage_bytes,
               self.n_stages, self.stage_order, self.status)
-        return sum(t.numel() * t.element_size() for t in ts)
+        return sum(t.numel() * t.element_size() for t in ts if t is not None)
 
     def host(self, b: int | None = None) -> list[PackedSchedule]:
         """Copy to host and split per matrix (synchronizes)."""
         h = {k: getattr(self, k).cpu().numpy() for k in (
             "balanced", "server", "move_count", "moves", "common_sum", "aux", "n_raw",
-            "stage_weight", "stage_perm", "stage_bytes", "n_stages", "stage_order", "status")}
+            "stage_weight", "stage_perm", "n_stages", "stage_order", "status")}
+        h["stage_bytes"] = None if self.stage_bytes is None else self.stage_bytes.cpu().numpy()
+        strip = None if self.strip is None else self.strip.cpu().numpy().view(STRIP_DTYPE)
         moves = h["moves"].view(MOVE_DTYPE).reshape(h["moves"].shape[:3])
         idx = range(self.B) if b is None else [b]
         out = []
         for i in idx:
             k, s = int(h["n_raw"][i]), int(h["n_stages"][i])
+            if h["stage_bytes"] is not None:
+                sb = h["stage_bytes"][i][:k]
+            else:
+                sb = stage_bytes_from_strip(h["stage_weight"][i][:k], h["stage_perm"][i][:k],
+                                            strip[i].reshape(-1))
             out.append(PackedSchedule(
                 n=self.n, m=self.m, status=int(h["status"][i]), balanced=h["balanced"][i],
                 server=h["server"][i], move_count=h["move_count"][i], moves=moves[i],
                 common_sum=int(h["common_sum"][i]), aux=h["aux"][i], n_raw=k,
                 stage_weight=h["stage_weight"][i][:k], stage_perm=h["stage_perm"][i][:k],
-                stage_bytes=h["stage_bytes"][i][:k], n_stages=s,
+                stage_bytes=sb, n_stages=s,
                 stage_order=h["stage_order"][i][:s]))
         return out
 
@@ -227,42 +244,85 @@ def decompose(embedded: np.ndarray) -> list[PermutationStage]:
     return list(p.raw_stages())
 
 
-_PACKED_FIELDS = ("balanced", "server", "move_count", "moves", "common_sum", "aux", "n_raw",
-                  "stage_weight", "stage_perm", "stage_bytes", "n_stages", "stage_order", "status")
+# fixed-size fields of the compact host result, copied whole per chunk
+_COMPACT_FIELDS = ("server", "move_count", "moves", "common_sum", "aux", "n_raw",
+                   "stage_weight", "stage_perm", "n_stages", "stage_order", "status", "strip",
+                   "tile_mask")
 
 
 class HostSchedules:
-    """Pinned host copy of a batch's packed schedules (same layout as
-    SynthBuffers), the output of synthesize_host_batch."""
+    """Compact pinned-host result of synthesize_host_batch for a batch.
 
-    def __init__(self, B: int, n: int, m: int):
-        like = SynthBuffers.__new__(SynthBuffers)  # shapes only
+    What crosses PCIe per matrix (config 5, n = 128, m = 8: ~5.9 MB instead
+    of the 37.7 MB full device layout): the server matrix, moves, aux, the
+    raw stage weights and permutations, the sort order, the aux run-out table
+    (`strip`, replaces the [K, n] stage_bytes array) and the balanced cross
+    tiles as changed-cell masks + values (`tile_mask`, `vals`; replaces the
+    G x G balanced matrix, which is D outside those cells).  ``packed(b, D)``
+    decodes one matrix into the full PackedSchedule (and thus the reference
+    dataclasses / canonical JSON)."""
+
+    def __init__(self, B: int, n: int, m: int, vals_capacity: int | None = None):
+        if m > 8:
+            raise ValidationError("the compact host layout needs m <= 8")
         G, T, S, K = n * m, n * (n - 1), max(m - 1, 1), stage_cap(n)
-        shapes = {"balanced": ((B, G, G), torch.int64), "server": ((B, n, n), torch.int64),
+        shapes = {"server": ((B, n, n), torch.int64),
                   "move_count": ((B, T), torch.int32), "moves": ((B, T, S, 2), torch.int64),
                   "common_sum": ((B,), torch.int64), "aux": ((B, n, n), torch.int64),
                   "n_raw": ((B,), torch.int32), "stage_weight": ((B, K), torch.int64),
-                  "stage_perm": ((B, K, n), torch.uint8), "stage_bytes": ((B, K, n), torch.int64),
-                  "n_stages": ((B,), torch.int32), "stage_order": ((B, K), torch.int32),
-                  "status": ((B,), torch.int32)}
-        del like
+                  "stage_perm": ((B, K, n), torch.uint8), "n_stages": ((B,), torch.int32),
+                  "stage_order": ((B, K), torch.int32), "status": ((B,), torch.int32),
+                  "strip": ((B, 2 * n + 2, 2), torch.int64),
+                  "tile_mask": ((B, max(T, 1)), torch.int64)}
         self.B, self.n, self.m = B, n, m
         for k, (shape, dt) in shapes.items():
             setattr(self, k, torch.empty(shape, dtype=dt, pin_memory=True))
+        self.val_base = torch.zeros(B + 1, dtype=torch.int64)
+        self.vals = torch.empty(int(vals_capacity or B * max(T, 1) * 16), dtype=torch.int64,
+                                pin_memory=True)
+        self.n_vals = 0
+
+    def fixed_nbytes(self) -> int:
+        return sum(getattr(self, k).numel() * getattr(self, k).element_size()
+                   for k in _COMPACT_FIELDS)
 
     def nbytes(self) -> int:
-        return sum(getattr(self, k).numel() * getattr(self, k).element_size() for k in _PACKED_FIELDS)
+        """Bytes copied device -> host by the last synthesize_host_batch."""
+        return self.fixed_nbytes() + 8 * self.n_vals + 8 * (self.B + 1)
+
+    def packed(self, b: int, D: np.ndarray) -> PackedSchedule:
+        """Decode matrix b (D: its host demand matrix) into the full layout."""
+        n, m = self.n, self.m
+        k, s = int(self.n_raw[b]), int(self.n_stages[b])
+        w = self.stage_weight[b, :k].numpy()
+        perm = self.stage_perm[b, :k].numpy()
+        strip = self.strip[b].numpy().view(STRIP_DTYPE).reshape(-1)
+        v0, v1 = int(self.val_base[b]), int(self.val_base[b + 1])
+        st = int(self.status[b])
+        bal = (balanced_from_compact(D, self.tile_mask[b].numpy().view(np.uint64),
+                                     self.vals[v0:v1].numpy(), n, m)
+               if st == 0 else np.array(D, dtype=np.int64))
+        moves = self.moves[b].numpy().view(MOVE_DTYPE).reshape(self.moves.shape[1:3])
+        return PackedSchedule(
+            n=n, m=m, status=st, balanced=bal, server=self.server[b].numpy(),
+            move_count=self.move_count[b].numpy(), moves=moves,
+            common_sum=int(self.common_sum[b]), aux=self.aux[b].numpy(), n_raw=k,
+            stage_weight=w, stage_perm=perm, stage_bytes=stage_bytes_from_strip(w, perm, strip),
+            n_stages=s, stage_order=self.stage_order[b, :s].numpy())
 
 
 def synthesize_host_batch(D_host: torch.Tensor, n: int, m: int, out: HostSchedules | None = None,
                           chunk: int = 125, device=None, _cache: dict = {}) -> HostSchedules:
-    """synthesize_fast over a batch held in (pinned) HOST memory.
+    """synthesize_fast over a batch held in (pinned) HOST memory, returning
+    the compact host result (HostSchedules).
 
     The batch is split into chunks, each on its own stream with its own
-    device buffers: chunk i's H2D, synthesis and D2H are stream-ordered, the
-    chunks are independent, so the copy engines stream the inputs and
-    results while every chunk's (latency-bound) decomposition runs
-    concurrently on the SMs.  Returns after the last D2H."""
+    device buffers: chunk i's H2D, synthesis (+ fast_compact_batch) and the
+    D2H of its fixed-size fields are stream-ordered; the chunks are
+    independent, so the copy engines stream inputs and results while every
+    chunk's (latency-bound) decomposition runs concurrently on the SMs.  The
+    variable-length changed-cell values of a chunk are copied once its count
+    has landed on the host.  Returns after the last D2H."""
     dev = device or _device()
     if D_host.device.type != "cpu" or D_host.dtype != torch.int64 or D_host.dim() != 3:
         raise ValidationError("D_host must be a CPU int64 tensor [B, G, G]")
@@ -271,26 +331,62 @@ def synthesize_host_batch(D_host: torch.Tensor, n: int, m: int, out: HostSchedul
     lib = _lib.load()
     C = max(1, min(chunk, B))
     starts = list(range(0, B, C))
+    T = n * (n - 1)
     key = (str(dev), B, n, m, C)
     if key not in _cache:  # device buffers and streams are reused across calls
         _cache.clear()
-        _cache[key] = ([SynthBuffers(min(C, B - b0), n, m, dev) for b0 in starts],
-                       [torch.empty((min(C, B - b0), n * m, n * m), dtype=torch.int64, device=dev)
-                        for b0 in starts],
-                       [torch.cuda.Stream(dev) for _ in starts])
-    bufs, dins, streams = _cache[key]
+        sizes = [min(C, B - b0) for b0 in starts]
+        _cache[key] = dict(
+            bufs=[SynthBuffers(nb, n, m, dev, stage_bytes=False, compact=True) for nb in sizes],
+            dins=[torch.empty((nb, n * m, n * m), dtype=torch.int64, device=dev) for nb in sizes],
+            vals=[torch.empty(nb * max(T, 1) * m * m, dtype=torch.int64, device=dev)
+                  for nb in sizes],
+            base=[torch.empty(nb + 1, dtype=torch.int64, device=dev) for nb in sizes],
+            base_h=[torch.empty(nb + 1, dtype=torch.int64, pin_memory=True) for nb in sizes],
+            ws=[torch.empty(int(lib.fast_compact_workspace_bytes(nb)), dtype=torch.uint8,
+                            device=dev) for nb in sizes],
+            streams=[torch.cuda.Stream(dev) for _ in starts],
+            events=[torch.cuda.Event() for _ in starts])
+    c = _cache[key]
     cur = torch.cuda.current_stream(dev)
     for i, b0 in enumerate(starts):
-        st, nb = streams[i], dins[i].shape[0]
+        st, nb, bufs = c["streams"][i], c["dins"][i].shape[0], c["bufs"][i]
         st.wait_stream(cur)
         with torch.cuda.stream(st):
-            dins[i].copy_(D_host[b0:b0 + nb], non_blocking=True)
-            rc = lib.fast_synth_batch(ctypes.c_void_p(dins[i].data_ptr()), nb, n, m,
-                                      ctypes.byref(bufs[i].struct), ctypes.c_void_p(st.cuda_stream))
-            _lib.check_rc(rc, "fast_synth_batch")
-            for f in _PACKED_FIELDS:
-                getattr(out, f)[b0:b0 + nb].copy_(getattr(bufs[i], f), non_blocking=True)
-    for st in streams:
+            c["dins"][i].copy_(D_host[b0:b0 + nb], non_blocking=True)
+            sh = ctypes.c_void_p(st.cuda_stream)
+            _lib.check_rc(lib.fast_synth_batch(ctypes.c_void_p(c["dins"][i].data_ptr()), nb, n, m,
+                                               ctypes.byref(bufs.struct), sh), "fast_synth_batch")
+            _lib.check_rc(lib.fast_compact_batch(ctypes.byref(bufs.struct), nb, n, m,
+                                                 ctypes.c_void_p(c["vals"][i].data_ptr()),
+                                                 ctypes.c_void_p(c["base"][i].data_ptr()),
+                                                 ctypes.c_void_p(c["ws"][i].data_ptr()), sh),
+                          "fast_compact_batch")
+            c["base_h"][i].copy_(c["base"][i], non_blocking=True)
+            c["events"][i].record(st)
+            for f in _COMPACT_FIELDS:
+                getattr(out, f)[b0:b0 + nb].copy_(getattr(bufs, f), non_blocking=True)
+    off = 0
+    for i, b0 in enumerate(starts):
+        c["events"][i].synchronize()
+        nb = c["dins"][i].shape[0]
+        base = c["base_h"][i]
+        tot = int(base[nb])
+        if off + tot > out.vals.numel():  # grow (first call at this size)
+            for st in c["streams"]:
+                st.synchronize()
+            grown = torch.empty(max(2 * out.vals.numel(), off + tot), dtype=torch.int64,
+                                pin_memory=True)
+            grown[:off].copy_(out.vals[:off])
+            out.vals = grown
+        with torch.cuda.stream(c["streams"][i]):
+            if tot:
+                out.vals[off:off + tot].copy_(c["vals"][i][:tot], non_blocking=True)
+        out.val_base[b0:b0 + nb] = base[:nb] + off
+        off += tot
+    out.val_base[B] = off
+    out.n_vals = off
+    for st in c["streams"]:
         st.synchronize()
     return out
 

@@ -89,3 +89,19 @@ def test_gpu_reproduces_reference_digest(n):
     for r, p in zip(recs, synth.synthesize_packed(D, n, m).host()):
         assert p.status == 0
         assert _sha(schedule_to_json(p.to_schedule()).encode()) == r["json_sha256"], r["seed"]
+    # compact layout (what the e2e path ships): device batch without the
+    # per-edge stage bytes, and the pinned-host compact result
+    for r, p in zip(recs, _compact_device(D, n, m).host()):
+        assert _sha(schedule_to_json(p.to_schedule()).encode()) == r["json_sha256"], r["seed"]
+    Dh = D.cpu().pin_memory()
+    hs = synth.synthesize_host_batch(Dh, n, m, chunk=3)
+    for b, r in enumerate(recs):
+        p = hs.packed(b, Dh[b].numpy())
+        assert _sha(schedule_to_json(p.to_schedule()).encode()) == r["json_sha256"], r["seed"]
+
+
+def _compact_device(D, n, m):
+    from paper_2505_09764_b200 import synth
+
+    bufs = synth.SynthBuffers(D.shape[0], n, m, D.device, stage_bytes=False, compact=True)
+    return synth.synthesize_packed(D, n, m, bufs)

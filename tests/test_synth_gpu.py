@@ -137,3 +137,46 @@ def test_gpu_deterministic_across_runs():
         assert pa.n_raw == pb.n_raw and pa.n_stages == pb.n_stages
         for k in ("stage_weight", "stage_perm", "stage_bytes", "stage_order", "balanced"):
             assert np.array_equal(getattr(pa, k), getattr(pb, k)), k
+
+
+def test_gpu_compact_layout_matches_golden(golden_schedules):
+    """The batch product layout (no per-edge stage bytes: the aux run-out
+    table; balanced tiles as changed-cell masks + values) decodes to the
+    reference's canonical JSON, on device and through the pinned-host path."""
+    groups = defaultdict(list)
+    for rec in golden_schedules:
+        if rec["m"] <= 8:
+            groups[(rec["n"], rec["m"])].append(rec)
+    total = 0
+    for (n, m), recs in groups.items():
+        Dn = np.array([r["D"] for r in recs], dtype=np.int64)
+        D = torch.tensor(Dn, device="cuda")
+        bufs = synth.SynthBuffers(len(recs), n, m, D.device, stage_bytes=False, compact=True)
+        packed = synth.synthesize_packed(D, n, m, bufs).host()
+        hs = synth.synthesize_host_batch(torch.from_numpy(Dn).pin_memory(), n, m, chunk=7)
+        for b, (rec, p) in enumerate(zip(recs, packed)):
+            assert p.status == 0, rec["name"]
+            assert schedule_to_json(p.to_schedule()) == rec["json"], rec["name"]
+            assert schedule_to_json(hs.packed(b, Dn[b]).to_schedule()) == rec["json"], rec["name"]
+            total += 1
+    assert total > 300
+
+
+@pytest.mark.parametrize("n,m", [(16, 8), (8, 8), (5, 3), (3, 1)])
+def test_gpu_compact_layout_matches_oracle(n, m):
+    rng = np.random.default_rng(7 * n + m)
+    B, G = 33, n * m
+    D = rng.integers(0, 1 << 30, size=(B, G, G), dtype=np.int64)
+    D[rng.random(D.shape) < 0.3] = 0
+    D[:, np.arange(G), np.arange(G)] = 0
+    ref = oracle.synthesize_batch(D, n, m)
+    hs = synth.synthesize_host_batch(torch.from_numpy(D).pin_memory(), n, m, chunk=10)
+    assert hs.nbytes() < synth.SynthBuffers(B, n, m, torch.device("cuda")).output_nbytes()
+    for b in range(B):
+        p = hs.packed(b, D[b])
+        want = oracle.packed_fields(ref, b, n, m)
+        for key in ("balanced", "server", "move_count", "aux", "stage_weight", "stage_perm",
+                    "stage_bytes", "stage_order"):
+            assert np.array_equal(getattr(p, key), want[key]), (key, b)
+        assert (p.status, p.common_sum, p.n_raw, p.n_stages) == (
+            want["status"], want["common_sum"], want["n_raw"], want["n_stages"]), b
