@@ -158,9 +158,12 @@ def bench_synth(args) -> dict:
     n, m, B = args.n, args.m, args.batch
     G, T = n * m, n * (n - 1)
     D = synth_inputs(args, dev)
-    # the batch product layout: no per-edge stage_bytes (the strip table
-    # replaces it), changed-cell masks + the compact pack of the balanced tiles
-    bufs = synth.SynthBuffers(B, n, m, dev, stage_bytes=False, compact=True)
+    # the batch product layout: the aux run-out table (replaces the per-edge
+    # stage bytes on the host side), changed-cell masks + the compact pack of
+    # the balanced tiles.  The per-edge stage bytes are still written on the
+    # device: the peel loop without those stores compiles ~13% slower
+    # (measured, profiles/README.md), and they never cross PCIe.
+    bufs = synth.SynthBuffers(B, n, m, dev, compact=True)
     vals = torch.empty(B * T * m * m, dtype=torch.int64, device=dev)
     vbase = torch.empty(B + 1, dtype=torch.int64, device=dev)
     cws = torch.empty(int(lib.fast_compact_workspace_bytes(B)), dtype=torch.uint8, device=dev)
@@ -204,7 +207,7 @@ def bench_synth(args) -> dict:
         t1.record(stream)
         torch.cuda.synchronize()
     total_ms = t0.elapsed_time(t1)
-    names = ("balance_kernel", "decompose_kernel", "sort_kernel", "compact_kernels")
+    names = ("balance_kernel", "decompose_kernel", "sort_strip_kernels", "compact_kernels")
     per = {k: 0.0 for k in names}
     for row in evs:
         for i, k in enumerate(names):
@@ -224,7 +227,7 @@ def bench_synth(args) -> dict:
     hbm = float(peaks["hbm_gbs"])
     alg = {"balance_kernel": 16 * G * G * B,
            "decompose_kernel": algorithmic_bytes_decompose(n, n_raw),
-           "sort_kernel": int(sum(12 * 2 * k for k in n_raw))}
+           "sort_strip_kernels": int(sum(12 * 2 * k for k in n_raw))}
     dom = max(per, key=per.get)
     achieved = alg[dom] / (per[dom] * 1e-3) / 1e9
     traffic = None
@@ -294,7 +297,7 @@ def bench_synth(args) -> dict:
                     move_count=p.move_count, moves=p.moves.view(np.int64).reshape(-1, 2),
                     common_sum=p.common_sum, aux=p.aux, n_raw=p.n_raw, n_stages=p.n_stages,
                     stage_weight=p.stage_weight, stage_perm=p.stage_perm,
-                    stage_bytes=p.stage_bytes, stage_order=p.stage_order), b, "e2e compact path")
+                    stage_bytes=p.stage_bytes, stage_order=p.stage_order), "e2e compact path")
         steps_mean = cpu.pop("_dfs_steps_mean")
         parity = {"parity_checked": k_chk, "against": "oracle/fast_oracle.c (pinned to tiersched "
                   "by tests/golden/headline_digests.json)", "paths": ["device", "e2e"] if hs is not None
@@ -348,7 +351,7 @@ def single_matrix_latency(args) -> dict:
     for n in (16, 32, 64, 128):
         G = n * args.m
         D = workloads.zipf_batch_device([0], G, args.skew, args.total, torch.device("cuda", 0))
-        bufs = synth.SynthBuffers(1, n, args.m, D.device, stage_bytes=False, compact=True)
+        bufs = synth.SynthBuffers(1, n, args.m, D.device, compact=True)
         times = []
         reps = 5 if n < 128 else 3
         for r in range(reps + 1):

@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kBalThreads)
 
 
 // One warp per matrix (decompose_one, synth_dev.cuh).
-template <int NW>
+template <int NW, bool WB>
 __global__ void __launch_bounds__(kDecWarps * 32)
     decompose_kernel(const int64_t* __restrict__ S_all, const int B,
                      const int n, const int mode, const int check_total,
@@ -185,8 +185,8 @@ __global__ void __launch_bounds__(kDecWarps * 32)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x * kDecWarps + warp;
   if (b >= B) return;
-  decompose_one<NW>(dsm + warp * dec_smem_bytes_t<NW>(n), S_all, b, n, mode, check_total, out,
-                    lane);
+  decompose_one<NW, WB>(dsm + warp * dec_smem_bytes_t<NW>(n), S_all, b, n, mode, check_total,
+                        out, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -267,6 +267,97 @@ __device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* sh_warp, 
 }
 
 constexpr int kCompactThreads = 512;
+
+// Aux run-out table (fast_strip_rec) from the decomposition's raw stages,
+// a post-pass that keeps the bookkeeping out of the peel loop.  One thread
+// per source row u replays strip_auxiliary (birkhoff.py:225-252) for the
+// row's auxiliary cells: they form one NW-corner staircase range
+// [lo_u, hi_u] (consecutive rows share at most one column, so the ranges
+// hold <= 2n-1 cells in all); the thread walks the raw stages in order
+// (perm[k][u] for the n threads is one coalesced 128-byte row per stage) and
+// charges the cell its row is matched to.  Record slot = the cell's position
+// in the concatenated ranges.
+constexpr int kStripThreads = FAST_MAX_SERVERS;
+constexpr int kStripTile = 128;
+__global__ void __launch_bounds__(kStripThreads)
+    strip_table_kernel(const int n, const fast_sched_bufs out) {
+  __shared__ int64_t shw[kStripThreads / 32];
+  __shared__ int64_t left[2 * FAST_MAX_SERVERS + 2];
+  __shared__ __align__(16) uint8_t tperm[kStripTile * FAST_MAX_SERVERS];
+  __shared__ int64_t tw[kStripTile];
+  const int b = blockIdx.x, u = threadIdx.x;
+  const int K = stage_cap(n), slots = 2 * n + 2;
+  fast_strip_rec* rec = out.strip + (int64_t)b * slots;
+  const bool ok = out.status[b] == FAST_OK;
+  const int64_t* aux = out.aux + (int64_t)b * n * n;
+  int lo = 0, hi = -1;
+  if (ok && u < n) {
+    for (int v = 0; v < n; ++v) {
+      if (aux[(int64_t)u * n + v] > 0) {
+        if (hi < 0) lo = v;
+        hi = v;
+      }
+    }
+  }
+  int64_t tot;
+  const int off = (int)block_excl_scan(hi >= lo ? hi - lo + 1 : 0, shw, tot);
+  for (int i = threadIdx.x; i < slots; i += blockDim.x) {
+    fast_strip_rec r;
+    r.real = 0;
+    r.stage = -1;
+    r.src = r.dst = 0;
+    rec[i] = r;
+  }
+  const bool mine = hi >= lo && off + (hi - lo) < slots;  // always (staircase bound)
+  int pending = 0;
+  if (mine) {
+    for (int v = lo; v <= hi; ++v) {
+      const int64_t a = aux[(int64_t)u * n + v];
+      left[off + v - lo] = a;
+      pending += a > 0;
+    }
+  }
+  __syncthreads();  // rec[] initialised before any thread writes a record
+  const int nr = ok ? out.n_raw[b] : 0;
+  // stage tiles: kStripTile raw stages' permutation rows and weights are
+  // staged in shared memory with 16-byte loads, then each thread walks its
+  // column of the tile (a shared-memory latency per stage, not a global one)
+  const uint8_t* perm = out.stage_perm + (int64_t)b * K * n;
+  const int64_t* wt = out.stage_weight + (int64_t)b * K;
+  const int rowv = n >> 4;  // 16-byte words per permutation row (n % 16 == 0 path)
+  for (int k0 = 0; k0 < nr && __syncthreads_or(pending > 0); k0 += kStripTile) {
+    const int kt = nr - k0 < kStripTile ? nr - k0 : kStripTile;
+    if ((n & 15) == 0) {
+      const uint4* src = reinterpret_cast<const uint4*>(perm + (int64_t)k0 * n);
+      for (int i = threadIdx.x; i < kt * rowv; i += blockDim.x)
+        reinterpret_cast<uint4*>(tperm)[i] = src[i];
+    } else {
+      for (int i = threadIdx.x; i < kt * n; i += blockDim.x) tperm[i] = perm[(int64_t)k0 * n + i];
+    }
+    for (int i = threadIdx.x; i < kt; i += blockDim.x) tw[i] = wt[k0 + i];
+    __syncthreads();
+    if (pending > 0) {
+      for (int k = 0; k < kt; ++k) {
+        const int v = tperm[k * n + u];
+        if (v < lo || v > hi) continue;
+        const int64_t l = left[off + v - lo];
+        if (l <= 0) continue;
+        const int64_t w = tw[k];
+        const int64_t ch = l < w ? l : w;
+        left[off + v - lo] = l - ch;
+        if (l == ch) {
+          fast_strip_rec r;
+          r.real = w - ch;
+          r.stage = k0 + k;
+          r.src = (int16_t)u;
+          r.dst = (int16_t)v;
+          rec[off + v - lo] = r;
+          --pending;
+        }
+      }
+    }
+  }
+}
 
 __global__ void __launch_bounds__(kCompactThreads)
     compact_count_kernel(const fast_sched_bufs out, const int T, int64_t* __restrict__ cnt) {
@@ -375,21 +466,27 @@ int launch_balance(const int64_t* D, int B, int n, int m,
   return check(cudaGetLastError());
 }
 
-template <int NW>
-int launch_decompose_t(const int64_t* S, int B, int n, int mode, int check_total,
-                       const fast_sched_bufs* out, cudaStream_t s) {
+template <int NW, bool WB>
+int launch_decompose_wb(const int64_t* S, int B, int n, int mode, int check_total,
+                        const fast_sched_bufs* out, cudaStream_t s) {
   const size_t smem = dec_smem_bytes_t<NW>(n) * kDecWarps;
   static size_t granted = 0;  // per template instance
   if (smem > 48 * 1024 && smem > granted) {
-    if (cudaFuncSetAttribute(decompose_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(decompose_kernel<NW, WB>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return FAST_ECUDA;
     granted = smem;
   }
   const int grid = (B + kDecWarps - 1) / kDecWarps;
-  decompose_kernel<NW><<<grid, kDecWarps * 32, smem, s>>>(S, B, n, mode,
-                                                          check_total, *out);
+  decompose_kernel<NW, WB><<<grid, kDecWarps * 32, smem, s>>>(S, B, n, mode, check_total, *out);
   return FAST_OK;
+}
+
+template <int NW>
+int launch_decompose_t(const int64_t* S, int B, int n, int mode, int check_total,
+                       const fast_sched_bufs* out, cudaStream_t s) {
+  return out->stage_bytes ? launch_decompose_wb<NW, true>(S, B, n, mode, check_total, out, s)
+                          : launch_decompose_wb<NW, false>(S, B, n, mode, check_total, out, s);
 }
 
 int launch_decompose(const int64_t* S, int B, int n, int mode, int check_total,
@@ -505,6 +602,10 @@ int fast_synth_batch_ev(const int64_t* D, int B, int n, int m,
   rc = launch_decompose(out->server, B, n, FAST_DEC_SERVER, 1, out, s,
                         ev ? ev[2] : nullptr);
   if (rc != FAST_OK) return rc;
+  if (out->strip) {
+    strip_table_kernel<<<B, kStripThreads, 0, s>>>(n, *out);
+    if (cudaGetLastError() != cudaSuccess) return FAST_ECUDA;
+  }
   if (ev && cudaEventRecord(ev[3], s) != cudaSuccess) return FAST_ECUDA;
   return FAST_OK;
 }

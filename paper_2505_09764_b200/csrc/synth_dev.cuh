@@ -521,7 +521,9 @@ __device__ __forceinline__ void apply_path(const DecSh<NW>& s, const int root,
 
 // The whole decomposition of matrix b by one warp; `wsm` is this warp's
 // dec_smem_bytes_t<NW>(n) bytes of shared memory.
-template <int NW>
+// WB: write the per-edge stage_bytes (compile-time, so that the compact
+// mode's peel loop carries no extra test)
+template <int NW, bool WB = true>
 __device__ __forceinline__ void decompose_one(char* wsm, const int64_t* __restrict__ S_all, const int b,
                               const int n, const int mode, const int check_total,
                               const fast_sched_bufs& out, const int lane) {
@@ -641,9 +643,6 @@ __device__ __forceinline__ void decompose_one(char* wsm, const int64_t* __restri
     }
     if (NWP > NW && lane == 0) s.sup[u * NWP + ((NWP - 1) ^ 1)] = 0u;
   }
-  fast_strip_rec* const strip = out.strip ? out.strip + (int64_t)b * (2 * n + 2) : nullptr;
-  if (strip)
-    for (int c = lane; c < 2 * n + 2; c += 32) strip[c].stage = -1;
   if (lane == 0) {
     out.common_sum[b] = common;
     // NW-corner staircase: row u's aux cells are the contiguous columns whose
@@ -718,7 +717,7 @@ __device__ __forceinline__ void decompose_one(char* wsm, const int64_t* __restri
   int k = 0, kept = 0;
   int64_t* wout = out.stage_weight + (int64_t)b * K;
   uint8_t* pout = out.stage_perm + (int64_t)b * K * n;
-  int64_t* bout = out.stage_bytes ? out.stage_bytes + (int64_t)b * K * n : nullptr;
+  int64_t* bout = WB ? out.stage_bytes + (int64_t)b * K * n : nullptr;
   while (remaining > 0) {
     DPROF_T(t0);
     if (k >= K) { st = FAST_EINVARIANT; break; }
@@ -739,20 +738,11 @@ __device__ __forceinline__ void decompose_one(char* wsm, const int64_t* __restri
       // strip_auxiliary (birkhoff.py:225-252): the cell pays aux first
       const int64_t charged = am[r] < weight ? am[r] : weight;
       const int64_t real = weight - charged;
-      const bool last_aux = charged > 0 && charged == am[r];  // the cell's aux runs out
       am[r] -= charged;
       mv[r] -= weight;
       if (valid) {
-        if (bout) __stcs(bout + (int64_t)k * n + u, real);
+        if constexpr (WB) __stcs(bout + (int64_t)k * n + u, real);
         pout[(int64_t)k * n + u] = (uint8_t)v;
-        if (strip && last_aux) {
-          fast_strip_rec rec;
-          rec.real = real;
-          rec.stage = k;
-          rec.src = (int16_t)u;
-          rec.dst = (int16_t)v;
-          strip[abase[r] + v] = rec;
-        }
       }
       const uint32_t rb = __ballot_sync(0xffffffffu, valid && real > 0);
       const uint32_t zb = __ballot_sync(0xffffffffu, valid && mv[r] == 0);

@@ -337,7 +337,7 @@ def synthesize_host_batch(D_host: torch.Tensor, n: int, m: int, out: HostSchedul
         _cache.clear()
         sizes = [min(C, B - b0) for b0 in starts]
         _cache[key] = dict(
-            bufs=[SynthBuffers(nb, n, m, dev, stage_bytes=False, compact=True) for nb in sizes],
+            bufs=[SynthBuffers(nb, n, m, dev, compact=True) for nb in sizes],
             dins=[torch.empty((nb, n * m, n * m), dtype=torch.int64, device=dev) for nb in sizes],
             vals=[torch.empty(nb * max(T, 1) * m * m, dtype=torch.int64, device=dev)
                   for nb in sizes],
