@@ -171,6 +171,7 @@ int fast_strip_sort(const int64_t *weight, const int16_t *dst, const int64_t *by
 #define FAST_PH_DIRECT 1       /* intra tile, or stage send of own bytes     */
 #define FAST_PH_FROM_STAGING 2 /* stage send of balanced-in bytes           */
 #define FAST_PH_REDIST 3       /* proxy staging -> final GPU (balance.py:210)*/
+#define FAST_STAGE_INTRA 255  /* fast_op.stage of an intra-server tile copy */
 #define FAST_BUF_SEND 0
 #define FAST_BUF_RECV 1
 #define FAST_BUF_STAGING 2
@@ -193,7 +194,8 @@ typedef struct {
   uint8_t src_buf;
   uint8_t dst_buf;
   uint8_t phase;
-  uint8_t stage; /* position in the ascending stage order */
+  uint8_t stage; /* position in the ascending stage order
+                    (FAST_STAGE_INTRA for intra-server tile copies) */
 } fast_op;
 
 /* Flag slots per rank available to one plan (fast_comm flags region). */
@@ -264,16 +266,29 @@ int64_t fast_comm_staging_capacity(const fast_comm *c);
 int fast_gather_demand(fast_comm *c, const int64_t *row, int64_t epoch,
                        void *stream);
 
+/* Measured per-phase timeline of one exec on one rank (%globaltimer ns;
+ * int64 [FAST_TIMELINE_STRIDE] per rank).  Windows are (first chunk start,
+ * last chunk end) over the chunks THIS rank executes; 0 / INT64_MAX-like
+ * sentinels (start = -1 as unsigned max) mean "no such chunk".  Mirrors the
+ * phase breakdown of the reference's Timeline (simulate.py:38-55). */
+#define FAST_TL_START 0        /* exec kernel start (CTA 0) */
+#define FAST_TL_BARRIER 1      /* entry barrier passed */
+#define FAST_TL_OWN_DONE 3     /* CTA 0 left the chunk loop */
+#define FAST_TL_RECV_DONE 4    /* every chunk addressed to this rank landed */
+#define FAST_TL_BALANCE 8      /* [8] start, [9] end: balance pushes */
+#define FAST_TL_INTRA 10       /* [10] start, [11] end: intra-server tiles */
+#define FAST_TL_STAGE0 16      /* [16 + 4k + 0/1] stage k sends (scale-out),
+                                  [16 + 4k + 2/3] stage k redistribution */
+#define FAST_TIMELINE_STRIDE (16 + 4 * 256)
+
 /* Execute a compiled plan: one persistent kernel per rank (`blocks` CTAs);
  * entry barrier, then producer CTAs run balance pushes, intra copies and
  * stage sends while a byte-proportional set of CTAs forwards redistribution
  * chunks as soon as their producer chunks have landed; chunk_bytes must be
  * the plan's.
  * On return (stream order) the local recv buffer holds the alltoallv
- * result.  timeline_ns (device int64[8 + 2*256] or NULL) receives
- * %globaltimer stamps: [0] start, [1] barrier passed, [2] balance arrivals
- * complete, [3] own ops done, [4] recv complete, [8+k] stage k arrivals at
- * this proxy complete. */
+ * result.  timeline_ns (device int64[FAST_TIMELINE_STRIDE] or NULL)
+ * receives the measured timeline above. */
 int fast_exec(fast_comm *c, const fast_plan *plan, const void *send,
               int64_t epoch, int blocks, int64_t chunk_bytes,
               int64_t *timeline_ns, void *stream); /* epoch 0: device counter */
@@ -281,7 +296,7 @@ int fast_exec(fast_comm *c, const fast_plan *plan, const void *send,
  * communicators whose symmetric blocks all live on the current device, and
  * one cooperative launch (grid = blocks x world, all CTAs co-resident) that
  * runs every rank's part of the plan.  sends: host array of `world` device
- * pointers.  timeline_ns: world x (8+256) int64 or NULL. */
+ * pointers.  timeline_ns: world x FAST_TIMELINE_STRIDE int64 or NULL. */
 int fast_comm_create_group(int world, int64_t recv_bytes, int64_t staging_bytes,
                            fast_comm **comms);
 int fast_exec_group(fast_comm *const *comms, int world, const fast_plan *plan,
@@ -313,6 +328,11 @@ int fast_comm_set_fused(fast_comm *c, int enable);
 int fast_comm_set_send_rows(fast_comm *c, const void *rows_base,
                             const int32_t *row_src, int64_t row_bytes,
                             int64_t n_rows);
+/* Bytes the executor may read from the send side (the send buffer, or
+ * n_rows * row_bytes of a row-mapped send); -1 (default) = unchecked.  Taken
+ * at enqueue time.  An op reaching past it makes the exec copy nothing and
+ * set status 2 (fast_comm_status). */
+int fast_comm_set_send_capacity(fast_comm *c, int64_t bytes);
 /* Number of calls issued through fast_alltoallv (the current epoch); callers
  * that drive fast_gather_demand / fast_exec themselves report theirs with
  * fast_comm_set_epoch so both paths share one monotone counter. */
@@ -328,8 +348,11 @@ void *fast_comm_peer_ptr(const fast_comm *c, int rank);
 int fast_debug_copy(void *dst, const void *src, int64_t bytes, int blocks,
                     int64_t chunk, int nc, void *stream);
 
-/* Device status word of the last exec on this comm (0 ok, 3 = a wait timed
- * out: peers missing or protocol error). */
+/* Device status word of the last exec on this comm: 0 ok, 2 = the counts
+ * overran the send capacity (fast_comm_set_send_capacity), 3 = a wait timed
+ * out (peers missing or protocol error).  A non-zero status is sticky and
+ * leaves the communicator's counters out of step with its peers: destroy
+ * and recreate the communicator on every rank. */
 int fast_comm_status(const fast_comm *c, int32_t *status_host);
 
 /* ------------------------------------------------------------------------
@@ -355,6 +378,15 @@ size_t fast_moe_route_workspace_bytes(int T, int k, int E);
 int fast_moe_route(const int32_t *topk, int T, int k, int E, int64_t row_bytes,
                    int32_t *pos, int64_t *counts, int64_t *seg_rows,
                    int64_t *demand_row, void *workspace, void *stream);
+
+/* fast_moe_route with E experts spread over E / experts_per_rank ranks
+ * (rank r hosts experts [r*L, (r+1)*L)): counts / seg_rows are per expert
+ * (the send layout is expert-major, hence rank-major), demand_row per rank.
+ * topk may come from a real router: ids outside [0, E) are rejected (the
+ * demand row is set to -1, so the alltoallv fails validation loudly). */
+int fast_moe_route_ex(const int32_t *topk, int T, int k, int E, int experts_per_rank,
+                      int64_t row_bytes, int32_t *pos, int64_t *counts, int64_t *seg_rows,
+                      int64_t *demand_row, void *workspace, void *stream);
 
 /* Pack: token t's row (row_bytes, 16-byte multiple) is copied to each of its
  * k destination rows of `send` (grouped by destination, stable token
@@ -396,6 +428,13 @@ int fast_moe_combine(const void *comb_recv, const void *expert_out,
                      int64_t row_bytes, const int32_t *topk, const int32_t *pos,
                      const void *workspace, int E, const int64_t *seg_rows,
                      const float *weights, void *out, void *stream);
+/* fast_moe_combine with E = G * experts_per_rank experts (fast_moe_route_ex). */
+int fast_moe_combine_ex(const void *comb_recv, const void *expert_out,
+                        const int64_t *Dfwd, int G, int rank, int T, int k,
+                        int64_t row_bytes, const int32_t *topk, const int32_t *pos,
+                        const void *workspace, int E, int experts_per_rank,
+                        const int64_t *seg_rows, const float *weights, void *out,
+                        void *stream);
 
 /* ------------------------------------------------------------------------
  * Analytical cost model, batched.  Replaces the

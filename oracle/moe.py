@@ -53,9 +53,11 @@ def pack(tokens: np.ndarray, topk: np.ndarray, E: int) -> np.ndarray:
     return tokens[order // k]
 
 
-def expert_inputs(tokens: list[np.ndarray], topks: list[np.ndarray], E: int) -> list[np.ndarray]:
-    """Expert input rows of every GPU h (source-major, self included)."""
-    G = len(tokens)
+def expert_inputs(tokens: list[np.ndarray], topks: list[np.ndarray], E: int,
+                  experts_per_rank: int = 1) -> list[np.ndarray]:
+    """Expert input rows of every GPU h (source-major, self included; within
+    a source, GPU h's experts h*L .. h*L+L-1 in order, tokens ascending)."""
+    G, L = len(tokens), experts_per_rank
     sends = [pack(tokens[s], topks[s], E) for s in range(G)]
     segs = [route(topks[s], E) for s in range(G)]
     out = []
@@ -63,7 +65,9 @@ def expert_inputs(tokens: list[np.ndarray], topks: list[np.ndarray], E: int) -> 
         parts = []
         for s in range(G):
             counts, seg, _ = segs[s]
-            parts.append(sends[s][seg[h]:seg[h] + counts[h]])
+            a = seg[h * L]
+            b = seg[h * L + L - 1] + counts[h * L + L - 1]
+            parts.append(sends[s][a:b])
         out.append(np.concatenate(parts))
     return out
 

@@ -62,6 +62,7 @@ SIGNATURES: list[tuple[str, object, list]] = [
     ("fast_comm_set_epoch", I, [V, I64]),
     ("fast_comm_set_fused", I, [V, I]),
     ("fast_comm_set_send_rows", I, [V, V, V, I64, I64]),
+    ("fast_comm_set_send_capacity", I, [V, I64]),
     ("fast_debug_copy", I, [V, V, I64, I, I64, I, V]),
     ("fast_comm_create_group", I, [I, I64, I64, ctypes.POINTER(V)]),
     ("fast_exec_group", I, [ctypes.POINTER(V), I, P_PLAN, ctypes.POINTER(V), I64, I, I64, V, V]),
@@ -82,4 +83,6 @@ SIGNATURES: list[tuple[str, object, list]] = [
     ("fast_moe_rowmap", I, [I, I, V, V, V, I, V, V, V]),
     ("fast_moe_unpack_self_rows", I, [V, V, I, I, V, V, I64, V, V]),
     ("fast_moe_combine", I, [V, V, V, I, I, I, I, I64, V, V, V, I, V, V, V, V]),
+    ("fast_moe_route_ex", I, [V, I, I, I, I, I64, V, V, V, V, V, V]),
+    ("fast_moe_combine_ex", I, [V, V, V, I, I, I, I, I64, V, V, V, I, I, V, V, V, V]),
 ]

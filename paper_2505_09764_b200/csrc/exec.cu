@@ -98,7 +98,8 @@ __device__ bool wait_geq(const uint64_t* p, uint64_t target, bool sys) {
 #define FAST_COPY_UNROLL 4  // 16-byte vectors in flight per thread per copy loop
 #endif
 constexpr int kMaxRanks = 16;       // one NVSwitch node
-constexpr int kTimelineStride = 8 + kMaxStages;
+constexpr int kTimelineStride = FAST_TIMELINE_STRIDE;
+static_assert(FAST_TIMELINE_STRIDE == FAST_TL_STAGE0 + 4 * kMaxStages, "timeline layout");
 
 struct ExecArgs {
   uint8_t* const* peers;  // [world] base of every rank's symmetric block
@@ -121,6 +122,7 @@ struct ExecArgs {
   int row_l;                    // ceil(log2(row_vec))
   const uint8_t* rows_bases[kMaxRanks];  // group mode: per local rank slot
   const int32_t* row_srcs[kMaxRanks];
+  int64_t send_cap;  // bytes readable from the send side (-1: unchecked)
 };
 
 __device__ __forceinline__ uint64_t* ctr(uint8_t* base, int idx) {
@@ -287,7 +289,11 @@ __device__ bool gather_rows(uint8_t* const* peers, const int64_t* row, int64_t e
     for (int r = 0; r < world; ++r) red_release_sys_add(ctr(peers[r], CTR_GATHER), 1);
     ok = wait_geq(ctr(peers[rank], CTR_GATHER), (uint64_t)epoch * world, true);
   }
-  return __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
+  const bool all_ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
+  // lane 0's acquire covers the peers' rows; __syncwarp orders the other
+  // lanes' later reads of them after it (a shuffle alone orders no memory)
+  __syncwarp();
+  return all_ok;
 }
 
 // epoch_in > 0: use it; 0: this call's epoch is the device counter + 1.
@@ -455,7 +461,17 @@ __device__ bool fused_prologue(const FusedArgs& f, uint8_t* const* peers, int ra
   if (tid == 0) *f.sched.status = FAST_OK;
   if (tl && tid == 0) tl[6] = (int64_t)globaltimer();
   __syncthreads();
-  if (!s_ok) return false;
+  if (!s_ok) {
+    // the other CTAs read the plan after GO: never leave them the previous
+    // call's op list
+    if (tid == 0) {
+      *f.pout.n_ops = 0;
+      *f.pout.status = FAST_EINVARIANT;
+      __threadfence();
+    }
+    __syncthreads();
+    return false;
+  }
   // build_balance_plan + reduce_to_server_level, one thread per tile
   const int TS = m * m + 1;
   const int slots = m > 1 ? m - 1 : 1;
@@ -493,7 +509,7 @@ __device__ bool fused_prologue(const FusedArgs& f, uint8_t* const* peers, int ra
     decompose_one<1>(dsm, f.sched.server, 0, n, FAST_DEC_SERVER, 1, f.sched, tid);
   __threadfence_block();
   __syncthreads();
-  if (tl && tid == 0) tl[8 + 250] = (int64_t)globaltimer();
+  if (tl && tid == 0) tl[12] = (int64_t)globaltimer();
   const int st = *f.sched.status;
   fastplan::PlanOut out = f.pout;
   if (st != FAST_OK) {
@@ -546,6 +562,14 @@ __global__ void __launch_bounds__(kExecThreads) exec_kernel(ExecArgs a, FusedArg
     __syncthreads();
   }
 
+  // measured timeline: open every window (start = max, end = 0) before the
+  // barrier releases the other CTAs
+  if (a.timeline && blockIdx.x == 0) {
+    uint64_t* t = reinterpret_cast<uint64_t*>(a.timeline);
+    for (int i = FAST_TL_BALANCE + tid; i < kTimelineStride; i += blockDim.x)
+      if (i < 12 || i >= FAST_TL_STAGE0) t[i] = ((i & 1) == 0) ? ~0ull : 0ull;
+    __syncthreads();
+  }
   // ---- entry barrier (CTA 0): reset the recv counter, arrive everywhere ---
   if (blockIdx.x == 0 && tid == 0) {
     if (a.timeline) a.timeline[0] = (int64_t)globaltimer();
@@ -568,6 +592,19 @@ __global__ void __launch_bounds__(kExecThreads) exec_kernel(ExecArgs a, FusedArg
   if (tid < 3) s_red[tid] = 0ull;
   __syncthreads();
   const int nops = (*a.plan_status == FAST_OK) ? *a.n_ops : 0;
+  // send-side bounds: the counts must fit the caller's send buffer
+  if (a.send_cap >= 0) {
+    bool over = false;
+    for (int i = tid; i < nops; i += blockDim.x) {
+      const fast_op o = a.ops[i];
+      over |= o.exec_rank == a.rank && o.src_buf == FAST_BUF_SEND &&
+              o.src_off + o.len > a.send_cap;
+    }
+    if (__syncthreads_or(over)) {
+      if (tid == 0) s_fail = 2;  // validation: nothing is copied
+      __syncthreads();
+    }
+  }
   {
     unsigned long long rc = 0, pb = 0, rb = 0;
     for (int i = tid; i < nops; i += blockDim.x) {
@@ -637,6 +674,8 @@ __global__ void __launch_bounds__(kExecThreads) exec_kernel(ExecArgs a, FusedArg
       __syncthreads();
       if (s_fail) break;
     }
+    uint64_t t_chunk = 0;
+    if (a.timeline && tid == 0) t_chunk = globaltimer();
     if (o.src_buf == FAST_BUF_SEND && a.row_src)
       cta_copy_rows(dst + off, o.src_off + off, len, a);
     else
@@ -646,6 +685,15 @@ __global__ void __launch_bounds__(kExecThreads) exec_kernel(ExecArgs a, FusedArg
       __threadfence_system();
       if (o.sig_slot >= 0) st_release_sys(slot_flag(peer, o.sig_slot + c), epoch);
       else red_release_sys_add(ctr(peer, CTR_RECV), 1);
+      if (a.timeline) {  // (first start, last end) of this chunk's phase window
+        int w;
+        if (o.phase == FAST_PH_BALANCE) w = FAST_TL_BALANCE;
+        else if (o.stage == FAST_STAGE_INTRA) w = FAST_TL_INTRA;
+        else w = FAST_TL_STAGE0 + 4 * o.stage + (o.phase == FAST_PH_REDIST ? 2 : 0);
+        unsigned long long* t = reinterpret_cast<unsigned long long*>(a.timeline) + w;
+        atomicMin(t, (unsigned long long)t_chunk);
+        atomicMax(t + 1, (unsigned long long)globaltimer());
+      }
     }
   }
   __syncthreads();
@@ -656,7 +704,11 @@ __global__ void __launch_bounds__(kExecThreads) exec_kernel(ExecArgs a, FusedArg
     if (a.timeline) a.timeline[4] = (int64_t)globaltimer();
   }
   __syncthreads();
-  if (tid == 0 && s_fail) atomicExch(reinterpret_cast<unsigned long long*>(status), 3ull);
+  // status word: 3 = a wait timed out (protocol), 2 = the counts overrun the
+  // send buffer.  Either leaves the communicator's counters out of step with
+  // its peers: it must be recreated (FastComm.check raises).
+  if (tid == 0 && s_fail)
+    atomicMax(reinterpret_cast<unsigned long long*>(status), s_fail == 2 ? 2ull : 3ull);
 }
 
 }  // namespace
@@ -677,6 +729,7 @@ struct fast_comm {
   const int32_t* row_src;
   uint32_t row_vec, row_magic;
   int row_l;
+  int64_t send_cap;  // fast_comm_set_send_capacity (-1: unchecked)
 };
 
 static void set_rowmap(ExecArgs& a, const fast_comm* c) {
@@ -787,6 +840,7 @@ int fast_comm_create(int rank, int world, int max_gpus_per_row, int64_t recv_byt
     return FAST_EVALIDATION;
   fast_comm* c = (fast_comm*)calloc(1, sizeof(fast_comm));
   if (!c) return FAST_ECUDA;
+  c->send_cap = -1;
   c->rank = rank;
   c->world = world;
   c->recv_bytes = recv_bytes;
@@ -922,6 +976,7 @@ static int exec_launch(fast_comm* c, const fast_plan* plan, const void* send, in
   a.world = c->world;
   a.skip_barrier = skip_barrier;
   set_rowmap(a, c);
+  a.send_cap = c->send_cap;
   FusedArgs f;
   memset(&f, 0, sizeof(f));
   exec_kernel<false><<<blocks, kExecThreads, 0, (cudaStream_t)stream>>>(a, f);
@@ -978,6 +1033,7 @@ int fast_exec_group(fast_comm* const* comms, int world, const fast_plan* plan,
   a.timeline = timeline_ns;
   a.rank = 0;
   a.world = world;
+  a.send_cap = -1;
   FusedArgs f;
   memset(&f, 0, sizeof(f));
   void* args[] = {&a, &f};
@@ -1041,6 +1097,7 @@ static int launch_fused(fast_comm* c, const void* send, const int64_t* counts, i
   a.world = c->world;
   a.skip_barrier = 1;  // the in-kernel demand all-gather synchronises the ranks
   set_rowmap(a, c);
+  a.send_cap = c->send_cap;
   FusedArgs f;
   memset(&f, 0, sizeof(f));
   f.counts = counts;
@@ -1094,6 +1151,12 @@ int fast_alltoallv(fast_comm* c, const void* send, const int64_t* counts, int n,
                          c->staging_bytes, chunk_bytes, plan, stream);
   if (rc != FAST_OK) return rc;
   return exec_launch(c, plan, send, 0, blocks, chunk_bytes, timeline_ns, stream, 1);
+}
+
+int fast_comm_set_send_capacity(fast_comm* c, int64_t bytes) {
+  if (!c) return FAST_EVALIDATION;
+  c->send_cap = bytes < 0 ? -1 : bytes;
+  return FAST_OK;
 }
 
 int fast_comm_set_send_rows(fast_comm* c, const void* rows_base, const int32_t* row_src,

@@ -61,15 +61,24 @@ __global__ void moe_gate_kernel(int T, uint64_t seed, int E, const uint64_t* __r
 
 // entries i = t*k + j in token order; pos[i] <- rank of i among the block's
 // entries with the same destination; blk[b][e] <- block totals
+// Router-provided top-k ids are validated here: an id outside [0, E) is
+// ignored by the histogram and raises `bad` (the scan then poisons the
+// demand row, so the alltoallv fails validation instead of dropping tokens).
 __global__ void __launch_bounds__(kRouteThreads)
     moe_route_local_kernel(const int32_t* __restrict__ topk, int N, int E,
-                           int32_t* __restrict__ pos, int32_t* __restrict__ blk) {
+                           int32_t* __restrict__ pos, int32_t* __restrict__ blk,
+                           int32_t* __restrict__ bad) {
   __shared__ int32_t wcnt[kRouteThreads / 32][kMaxExperts];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int i = tid; i < (kRouteThreads / 32) * E; i += blockDim.x) (&wcnt[0][0])[(i / E) * kMaxExperts + i % E] = 0;
   __syncthreads();
   const int i = blockIdx.x * blockDim.x + tid;
-  const int e = i < N ? topk[i] : -1;
+  int e = i < N ? topk[i] : -1;
+  if (i < N && (e < 0 || e >= E)) {
+    atomicOr(bad, 1);
+    e = -1;
+    pos[i] = -1;
+  }
   const unsigned peers = __match_any_sync(0xffffffffu, e);
   const int lrank = __popc(peers & ((1u << lane) - 1u));
   if (e >= 0 && lrank == 0) wcnt[warp][e] = __popc(peers);
@@ -92,9 +101,9 @@ __global__ void __launch_bounds__(kRouteThreads)
 // parallel, warp exclusive scan + carry (no dependent global-load chain)
 constexpr int kScanThreads = 1024;
 __global__ void __launch_bounds__(kScanThreads)
-    moe_route_scan_kernel(int nblocks, int E, int64_t row_bytes, int32_t* __restrict__ blk,
-                          int64_t* __restrict__ counts, int64_t* __restrict__ seg_rows,
-                          int64_t* __restrict__ demand_row) {
+    moe_route_scan_kernel(int nblocks, int E, int L, int64_t row_bytes, int32_t* __restrict__ blk,
+                          const int32_t* __restrict__ bad, int64_t* __restrict__ counts,
+                          int64_t* __restrict__ seg_rows, int64_t* __restrict__ demand_row) {
   __shared__ int64_t s_cnt[kMaxExperts];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int e = warp; e < E; e += kScanThreads / 32) {
@@ -114,7 +123,6 @@ __global__ void __launch_bounds__(kScanThreads)
     if (lane == 0) {
       s_cnt[e] = run;
       counts[e] = run;
-      demand_row[e] = run * row_bytes;
     }
   }
   __syncthreads();
@@ -123,6 +131,13 @@ __global__ void __launch_bounds__(kScanThreads)
     for (int x = 0; x < E; ++x) {
       seg_rows[x] = a;
       a += s_cnt[x];
+    }
+    // demand row per destination rank: its L consecutive experts
+    const bool poisoned = *bad != 0;
+    for (int r = 0; r < E / L; ++r) {
+      int64_t c = 0;
+      for (int x = r * L; x < (r + 1) * L; ++x) c += s_cnt[x];
+      demand_row[r] = poisoned ? -1 : c * row_bytes;
     }
   }
 }
@@ -155,8 +170,11 @@ __global__ void __launch_bounds__(256)
     for (int j = 0; j < K; ++j) {
       const int i = t * K + j;
       const int e = topk[i];
-      const int64_t row = seg_rows[e] + blkbase[(int64_t)(i / kRouteThreads) * E + e] + pos[i];
-      dst[j] = send + row * row_vec;
+      // an invalid id (rejected by the route) is not written anywhere
+      dst[j] = (e < 0 || e >= E)
+                   ? nullptr
+                   : send + (seg_rows[e] + blkbase[(int64_t)(i / kRouteThreads) * E + e] + pos[i]) *
+                                row_vec;
     }
     const uint4* src = tokens + (int64_t)t * row_vec;
     constexpr int U = 4;
@@ -168,12 +186,14 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int j = 0; j < K; ++j)
 #pragma unroll
-        for (int u = 0; u < U; ++u) stg_na(dst[j] + v + u * 32, x[u]);
+        for (int u = 0; u < U; ++u)
+          if (dst[j]) stg_na(dst[j] + v + u * 32, x[u]);
     }
     for (; v < row_vec; v += 32) {
       const uint4 x = ldg_nc(src + v);
 #pragma unroll
-      for (int j = 0; j < K; ++j) stg_na(dst[j] + v, x);
+      for (int j = 0; j < K; ++j)
+        if (dst[j]) stg_na(dst[j] + v, x);
     }
   }
 }
@@ -189,6 +209,7 @@ __global__ void moe_rowmap_kernel(int T, const int32_t* __restrict__ topk,
                                   int32_t* __restrict__ row_src) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < T * K; i += gridDim.x * blockDim.x) {
     const int e = topk[i];
+    if (e < 0 || e >= E) continue;  // rejected by the route
     row_src[seg_rows[e] + blkbase[(int64_t)(i / kRouteThreads) * E + e] + pos[i]] = i / K;
   }
 }
@@ -259,7 +280,7 @@ __global__ void __launch_bounds__(256)
                        const uint8_t* __restrict__ expert_out, const int64_t* __restrict__ Dfwd,
                        int G, int me, int T, int64_t row_vec, const int32_t* __restrict__ topk,
                        const int32_t* __restrict__ pos, const int32_t* __restrict__ blkbase,
-                       int E, const int64_t* __restrict__ seg_rows,
+                       int E, int L, const int64_t* __restrict__ seg_rows,
                        const float* __restrict__ weights, uint4* __restrict__ out) {
   __shared__ int64_t s_self_off;
   if (threadIdx.x == 0) {
@@ -267,6 +288,7 @@ __global__ void __launch_bounds__(256)
     for (int g = 0; g < me; ++g) o += Dfwd[(int64_t)g * G + me];
     s_self_off = o;
   }
+  const int64_t self_row0 = seg_rows[me * L];  // first send row of my experts
   __syncthreads();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -280,8 +302,9 @@ __global__ void __launch_bounds__(256)
       const int i = t * K + j;
       const int e = topk[i];
       const int64_t r = blkbase[(int64_t)(i / kRouteThreads) * E + e] + pos[i];
-      src[j] = (e == me)
-                   ? reinterpret_cast<const uint4*>(expert_out + s_self_off + r * RB)
+      src[j] = (e / L == me)
+                   ? reinterpret_cast<const uint4*>(expert_out + s_self_off +
+                                                    (seg_rows[e] - self_row0 + r) * RB)
                    : reinterpret_cast<const uint4*>(comb_recv + (seg_rows[e] + r) * RB);
       w[j] = weights[i];
     }
@@ -323,7 +346,11 @@ size_t fast_moe_route_workspace_bytes(int T, int k, int E) {
   if (T < 0 || k < 1 || E < 1) return 0;
   const int64_t N = (int64_t)T * k;
   const int64_t nb = (N + kRouteThreads - 1) / kRouteThreads;
-  return (size_t)((nb > 0 ? nb : 1) * E * 4);
+  return (size_t)((nb > 0 ? nb : 1) * E * 4) + 16;  // + the invalid-id flag
+}
+
+static int32_t* route_bad_flag(void* workspace, int T, int k, int E) {
+  return (int32_t*)((char*)workspace + fast_moe_route_workspace_bytes(T, k, E) - 16);
 }
 
 int fast_moe_gate(int T, uint64_t seed, int E, const uint64_t* thr, const uint64_t* thr2,
@@ -335,20 +362,31 @@ int fast_moe_gate(int T, uint64_t seed, int E, const uint64_t* thr, const uint64
   return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
 }
 
-int fast_moe_route(const int32_t* topk, int T, int k, int E, int64_t row_bytes, int32_t* pos,
-                   int64_t* counts, int64_t* seg_rows, int64_t* demand_row, void* workspace,
-                   void* stream) {
-  if (T < 0 || k < 1 || E < 1 || E > kMaxExperts || row_bytes < 0 || !counts || !seg_rows ||
-      !demand_row || !workspace)
+int fast_moe_route_ex(const int32_t* topk, int T, int k, int E, int experts_per_rank,
+                      int64_t row_bytes, int32_t* pos, int64_t* counts, int64_t* seg_rows,
+                      int64_t* demand_row, void* workspace, void* stream) {
+  const int L = experts_per_rank;
+  if (T < 0 || k < 1 || E < 1 || E > kMaxExperts || L < 1 || E % L || row_bytes < 0 ||
+      !counts || !seg_rows || !demand_row || !workspace)
     return FAST_EVALIDATION;
   cudaStream_t s = (cudaStream_t)stream;
   const int N = T * k;
   const int nb = N > 0 ? (N + kRouteThreads - 1) / kRouteThreads : 0;
+  int32_t* bad = route_bad_flag(workspace, T, k, E);
+  if (cudaMemsetAsync(bad, 0, 4, s) != cudaSuccess) return FAST_ECUDA;
   if (nb > 0)
-    moe_route_local_kernel<<<nb, kRouteThreads, 0, s>>>(topk, N, E, pos, (int32_t*)workspace);
-  moe_route_scan_kernel<<<1, kScanThreads, 0, s>>>(nb, E, row_bytes, (int32_t*)workspace, counts,
-                                         seg_rows, demand_row);
+    moe_route_local_kernel<<<nb, kRouteThreads, 0, s>>>(topk, N, E, pos, (int32_t*)workspace,
+                                                        bad);
+  moe_route_scan_kernel<<<1, kScanThreads, 0, s>>>(nb, E, L, row_bytes, (int32_t*)workspace, bad,
+                                                   counts, seg_rows, demand_row);
   return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
+}
+
+int fast_moe_route(const int32_t* topk, int T, int k, int E, int64_t row_bytes, int32_t* pos,
+                   int64_t* counts, int64_t* seg_rows, int64_t* demand_row, void* workspace,
+                   void* stream) {
+  return fast_moe_route_ex(topk, T, k, E, 1, row_bytes, pos, counts, seg_rows, demand_row,
+                           workspace, stream);
 }
 
 int fast_moe_pack(const void* tokens, int T, int k, int64_t row_bytes, const int32_t* topk,
@@ -420,9 +458,19 @@ int fast_moe_combine(const void* comb_recv, const void* expert_out, const int64_
                      int rank, int T, int k, int64_t row_bytes, const int32_t* topk,
                      const int32_t* pos, const void* workspace, int E, const int64_t* seg_rows,
                      const float* weights, void* out, void* stream) {
+  return fast_moe_combine_ex(comb_recv, expert_out, Dfwd, G, rank, T, k, row_bytes, topk, pos,
+                             workspace, E, 1, seg_rows, weights, out, stream);
+}
+
+int fast_moe_combine_ex(const void* comb_recv, const void* expert_out, const int64_t* Dfwd,
+                        int G, int rank, int T, int k, int64_t row_bytes, const int32_t* topk,
+                        const int32_t* pos, const void* workspace, int E, int experts_per_rank,
+                        const int64_t* seg_rows, const float* weights, void* out, void* stream) {
+  const int L = experts_per_rank;
   if (T < 0 || (k != 1 && k != 2 && k != 4 && k != 8) || row_bytes <= 0 || (row_bytes & 15) ||
       !comb_recv || !expert_out || !Dfwd || !topk || !pos || !workspace || !seg_rows ||
-      !weights || !out || rank < 0 || rank >= G || ((uintptr_t)out & 15))
+      !weights || !out || rank < 0 || rank >= G || ((uintptr_t)out & 15) || L < 1 ||
+      E != G * L)
     return FAST_EVALIDATION;
   if (T == 0) return FAST_OK;
   int blocks = (int)(((int64_t)T * 32 + 255) / 256);
@@ -434,10 +482,10 @@ int fast_moe_combine(const void* comb_recv, const void* expert_out, const int64_
   const int32_t* bb = (const int32_t*)workspace;
   uint4* o = (uint4*)out;
   switch (k) {
-    case 1: moe_combine_kernel<1><<<blocks, 256, 0, s>>>(cr, eo, Dfwd, G, rank, T, rv, topk, pos, bb, E, seg_rows, weights, o); break;
-    case 2: moe_combine_kernel<2><<<blocks, 256, 0, s>>>(cr, eo, Dfwd, G, rank, T, rv, topk, pos, bb, E, seg_rows, weights, o); break;
-    case 4: moe_combine_kernel<4><<<blocks, 256, 0, s>>>(cr, eo, Dfwd, G, rank, T, rv, topk, pos, bb, E, seg_rows, weights, o); break;
-    default: moe_combine_kernel<8><<<blocks, 256, 0, s>>>(cr, eo, Dfwd, G, rank, T, rv, topk, pos, bb, E, seg_rows, weights, o); break;
+    case 1: moe_combine_kernel<1><<<blocks, 256, 0, s>>>(cr, eo, Dfwd, G, rank, T, rv, topk, pos, bb, E, L, seg_rows, weights, o); break;
+    case 2: moe_combine_kernel<2><<<blocks, 256, 0, s>>>(cr, eo, Dfwd, G, rank, T, rv, topk, pos, bb, E, L, seg_rows, weights, o); break;
+    case 4: moe_combine_kernel<4><<<blocks, 256, 0, s>>>(cr, eo, Dfwd, G, rank, T, rv, topk, pos, bb, E, L, seg_rows, weights, o); break;
+    default: moe_combine_kernel<8><<<blocks, 256, 0, s>>>(cr, eo, Dfwd, G, rank, T, rv, topk, pos, bb, E, L, seg_rows, weights, o); break;
   }
   return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
 }

@@ -322,7 +322,7 @@ FAST_HD inline void plan_compile(const PlanIn& in, const PlanOut& out) {
         const int g = i * m + p, h = i * m + q;
         const int64_t len = in.D[(int64_t)g * G + h];
         if (g != h && len > 0)
-          sk.push(1, make_op(FAST_PH_DIRECT, 0, g, FAST_BUF_SEND, w.send_off[(int64_t)g * G + h],
+          sk.push(1, make_op(FAST_PH_DIRECT, FAST_STAGE_INTRA, g, FAST_BUF_SEND, w.send_off[(int64_t)g * G + h],
                              h, FAST_BUF_RECV, w.recv_off[(int64_t)g * G + h], len));
       }
 

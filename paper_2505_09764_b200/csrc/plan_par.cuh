@@ -450,7 +450,7 @@ __device__ __forceinline__ void plan_compile_par(const PlanIn& in, const PlanOut
       const int h = i * m + q;
       const int64_t len = in.D[(int64_t)g * G + h];
       if (h != g && len > 0)
-        out.ops[at++] = make_op(FAST_PH_DIRECT, 0, g, FAST_BUF_SEND, w.send_off[(int64_t)g * G + h],
+        out.ops[at++] = make_op(FAST_PH_DIRECT, FAST_STAGE_INTRA, g, FAST_BUF_SEND, w.send_off[(int64_t)g * G + h],
                                 h, FAST_BUF_RECV, w.recv_off[(int64_t)g * G + h], len);
     }
   }

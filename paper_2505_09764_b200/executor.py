@@ -36,7 +36,9 @@ OP_DTYPE = np.dtype([("src_off", "<i8"), ("dst_off", "<i8"), ("len", "<i8"),
                      ("dst_buf", "u1"), ("phase", "u1"), ("stage", "u1")])
 PH_BALANCE, PH_DIRECT, PH_FROM_STAGING, PH_REDIST = 0, 1, 2, 3
 BUF_SEND, BUF_RECV, BUF_STAGING = 0, 1, 2
-TIMELINE_STRIDE = 8 + 256
+TIMELINE_STRIDE = 16 + 4 * 256  # FAST_TIMELINE_STRIDE (include/fastb200.h)
+TL_START, TL_BARRIER, TL_RECV_DONE, TL_BALANCE, TL_INTRA, TL_STAGE0 = 0, 1, 4, 8, 10, 16
+STAGE_INTRA = 255
 DEFAULT_BLOCKS = 128  # one 512-thread CTA per SM; must stay <= SM count (co-residency)
 DEFAULT_CHUNK = 1024 * 1024
 
@@ -102,15 +104,47 @@ def plan_compile_host(D: np.ndarray, n: int, m: int, order: np.ndarray, perm: np
     return ops[: int(n_ops[0])].copy(), used, int(st)
 
 
+_NO_START = (1 << 64) - 1
+
+
+def phase_windows(stamps: np.ndarray, n_stages: int) -> dict:
+    """Measured (start, end) windows in seconds since the exec kernel's start,
+    from one rank's timeline stamps (FAST_TL_* in include/fastb200.h); None
+    for a phase this rank executed no chunk of."""
+    u = stamps.astype(np.uint64)
+    t0 = int(u[TL_START])
+
+    def win(i):
+        a, b = int(u[i]), int(u[i + 1])
+        if a == _NO_START or b == 0:
+            return None
+        return ((a - t0) * 1e-9, (b - t0) * 1e-9)
+
+    return {"barrier": (int(u[TL_BARRIER]) - t0) * 1e-9,
+            "recv_done": (int(u[TL_RECV_DONE]) - t0) * 1e-9,
+            "balance": win(TL_BALANCE), "intra": win(TL_INTRA),
+            "scale_out": [win(TL_STAGE0 + 4 * k) for k in range(n_stages)],
+            "redistribution": [win(TL_STAGE0 + 4 * k + 2) for k in range(n_stages)]}
+
+
+def _n_stages_of(ops: np.ndarray | None) -> int:
+    if ops is None or not len(ops):
+        return 0
+    st = ops["stage"][ops["stage"] != STAGE_INTRA]
+    return int(st.max()) + 1 if len(st) else 0
+
+
 def _timeline_from(stamps: np.ndarray, ops: np.ndarray | None, rank: int) -> Timeline:
-    t0 = stamps[1]
-    sec = lambda x: max(0.0, (int(x) - int(t0)) * 1e-9) if x else 0.0  # noqa: E731
-    n_st = 0
-    if ops is not None and len(ops):
-        n_st = int(ops["stage"].max()) + 1
-    so = tuple(sec(stamps[8 + k]) for k in range(n_st))
-    return Timeline(t_balance=sec(stamps[2]), t_intra_a2a=0.0, scale_out=so,
-                    redistribution=tuple(0.0 for _ in so), total=sec(stamps[4]))
+    """Measured Timeline of one rank (the reference's phase breakdown,
+    simulate.py:38-55): each phase's duration is its window on this rank
+    (first chunk start to last chunk end); total = exec start -> every byte
+    addressed to this rank has landed."""
+    w = phase_windows(stamps, _n_stages_of(ops))
+    dur = lambda x: 0.0 if x is None else max(0.0, x[1] - x[0])  # noqa: E731
+    return Timeline(t_balance=dur(w["balance"]), t_intra_a2a=dur(w["intra"]),
+                    scale_out=tuple(dur(x) for x in w["scale_out"]),
+                    redistribution=tuple(dur(x) for x in w["redistribution"]),
+                    total=max(0.0, w["recv_done"]))
 
 
 class FastComm:
@@ -156,6 +190,8 @@ class FastComm:
         self.use_graph = True
         self._fused = False
         self._graphs: dict = {}
+        self._count_cache: dict = {}
+        self._split_bad: torch.Tensor | None = None
 
     def set_fused(self, enable: bool) -> None:
         """Single-launch path (gather + synthesis + plan inside the exec
@@ -212,24 +248,29 @@ class FastComm:
                       "fast_comm_set_send_rows")
         try:
             return self._alltoallv(send, send_counts, stream, record_timeline, exec_events,
-                                   (rows.data_ptr(), row_src.data_ptr(), int(row_bytes)))
+                                   (rows.data_ptr(), row_src.data_ptr(), int(row_bytes)),
+                                   send_cap=int(row_src.numel()) * int(row_bytes))
         finally:
             lib.fast_comm_set_send_rows(self._ptr, None, None, 0, 0)
 
     def _alltoallv(self, send, send_counts, stream, record_timeline, exec_events,
-                   rows_key=None) -> torch.Tensor:
+                   rows_key=None, send_cap=None) -> torch.Tensor:
         lib = _lib.load()
         if send.dtype != torch.uint8 or not send.is_cuda:
             raise ValidationError("send must be a cuda uint8 tensor")
         n, m = self.topology.n_servers, self.topology.gpus_per_server
+        s = stream or torch.cuda.current_stream()
         row = send_counts
         if row.dtype != torch.int64 or row.device != self.device or not row.is_contiguous():
-            row = row.to(device=self.device, dtype=torch.int64).contiguous()
+            with torch.cuda.stream(s):  # converted on the stream that consumes it
+                row = row.to(device=self.device, dtype=torch.int64).contiguous()
         self._row = row  # keep alive until the stream consumes it
-        s = stream or torch.cuda.current_stream()
+        cap = int(send.numel()) if send_cap is None else int(send_cap)
+        _lib.check_rc(lib.fast_comm_set_send_capacity(self._ptr, cap), "set_send_capacity")
         tl = ctypes.c_void_p(self.timeline.data_ptr()) if record_timeline else None
         if exec_events is None:
-            key = (send.data_ptr(), row.data_ptr(), bool(record_timeline), self._fused, rows_key)
+            key = (send.data_ptr(), cap, row.data_ptr(), bool(record_timeline), self._fused,
+                   rows_key)
             g = self._graphs.get(key) if (self.use_graph and stream is None) else None
             if g is not None:  # one graph launch per call
                 g.replay()
@@ -290,46 +331,138 @@ class FastComm:
         plan_st = int(self.plan.status.item())
         if plan_st != 0:
             _lib.check_rc(plan_st, "fast_plan_compile")
+        if st.value == 2:
+            raise ValidationError("fast_exec: send counts overrun the send buffer "
+                                  "(recreate the communicator)")
         if st.value != 0:
-            _lib.check_rc(3, "fast_exec (timeout / protocol)")
+            _lib.check_rc(3, "fast_exec (timeout / protocol; recreate the communicator)")
+        if self._split_bad is not None and bool(self._split_bad.item()):
+            raise ValidationError("all_to_all_fast: output_split_sizes disagree with the "
+                                  "gathered send counts")
+
+    def _counts_for(self, splits: tuple, row_bytes: int, out: bool = False) -> torch.Tensor:
+        """Device int64 bytes-per-rank vector for a split tuple, cached (no
+        per-call host->device copy; stable pointers keep the call graphs)."""
+        key = (splits, int(row_bytes), out)
+        t = self._count_cache.get(key)
+        if t is None:
+            h = torch.tensor([int(x) * int(row_bytes) for x in splits], dtype=torch.int64)
+            t = h.pin_memory().to(self.device, non_blocking=True)
+            if len(self._count_cache) > 256:
+                self._count_cache.clear()
+            self._count_cache[key] = t
+        return t
+
+    def _check_output_splits(self, out_bytes: torch.Tensor) -> None:
+        """Device-side: the gathered column `rank` (bytes each source sends
+        here, own segment from the self sizes) must equal out_bytes; a
+        mismatch is recorded and raised by check()."""
+        r = self.rank
+        col = self.demand()[:, r].clone()
+        col[r] = self.self_sizes()[r]
+        bad = (col != out_bytes).any()
+        if self._split_bad is None:
+            self._split_bad = bad.clone()
+        else:
+            self._split_bad.logical_or_(bad)
 
     def measured_timeline(self) -> Timeline:
+        """Timeline of the last call made with record_timeline=True (syncs)."""
         return _timeline_from(self.timeline.cpu().numpy(), self.plan.host_ops(), self.rank)
 
+    def measured_phases(self) -> dict:
+        """(start, end) phase windows of the last recorded call (syncs)."""
+        return phase_windows(self.timeline.cpu().numpy(), _n_stages_of(self.plan.host_ops()))
 
-def all_to_all_fast(output: torch.Tensor, input: torch.Tensor,
+
+def all_to_all_fast(output: torch.Tensor | None, input: torch.Tensor,
                     output_split_sizes: list[int] | None = None,
                     input_split_sizes: list[int] | None = None,
-                    comm: FastComm | None = None) -> torch.Tensor:
+                    comm: FastComm | None = None, check_splits: bool = True) -> torch.Tensor:
     """Drop-in for torch.distributed.all_to_all_single on the
-    FAST path.  Splits are along dim 0 in rows; the self segment is a local
-    copy, everything else goes through comm.alltoallv."""
+    FAST path.  Splits are along dim 0 in rows.
+
+    The executor writes every remote segment straight into the
+    communicator's receive region, laid out exactly like all_to_all_single's
+    output with a gap at the own slot; the own segment is one local copy into
+    that gap.  ``output=None`` returns that region as the result (zero copy;
+    valid until the next call on `comm`); a caller-owned `output` receives one
+    contiguous device copy.  Split counts are cached on the device (no
+    per-call host->device copy).  check_splits: output_split_sizes are
+    compared on the device with the gathered send counts; a mismatch is
+    raised by comm.check()."""
     if comm is None:
         raise ValidationError("all_to_all_fast needs a FastComm")
     W = comm.world
-    rows_in, rows_out = input.shape[0], output.shape[0]
-    row_bytes = input[0].numel() * input.element_size() if rows_in else 0
+    rows_in = input.shape[0]
+    row_bytes = (input[0].numel() if rows_in else
+                 int(np.prod(input.shape[1:], dtype=np.int64))) * input.element_size()
     if input_split_sizes is None:
+        if rows_in % W:
+            raise ValidationError("input rows are not divisible by the world size")
         input_split_sizes = [rows_in // W] * W
     if output_split_sizes is None:
-        output_split_sizes = [rows_out // W] * W
-    inb = input.contiguous().view(torch.uint8).reshape(-1)
-    counts = torch.tensor([s * row_bytes for s in input_split_sizes], dtype=torch.int64,
-                          device=input.device)
-    recv = comm.alltoallv(inb, counts)
-    # recv is laid out like all_to_all_single's output with a gap at the self
-    # slot: one contiguous copy, then the local segment into its slot
-    outb = output.view(torch.uint8).reshape(-1)
-    r = comm.rank
+        if output is None:
+            raise ValidationError("output_split_sizes are needed without an output tensor")
+        if output.shape[0] % W:
+            raise ValidationError("output rows are not divisible by the world size")
+        output_split_sizes = [output.shape[0] // W] * W
+    if len(input_split_sizes) != W or len(output_split_sizes) != W:
+        raise ValidationError("split lists must have one entry per rank")
+    if sum(input_split_sizes) != rows_in:
+        raise ValidationError("input_split_sizes do not sum to the input rows")
     total_out = sum(output_split_sizes) * row_bytes
+    if total_out > comm.recv_bytes:
+        raise ValidationError("output larger than the communicator's receive region")
+    if output is not None and output.numel() * output.element_size() < total_out:
+        raise ValidationError("output tensor smaller than sum(output_split_sizes)")
+    inb = input.contiguous().view(torch.uint8).reshape(-1)
+    counts = comm._counts_for(tuple(input_split_sizes), row_bytes)
+    recv = comm.alltoallv(inb, counts)
+    r = comm.rank
     self_in = sum(input_split_sizes[:r]) * row_bytes
     self_out = sum(output_split_sizes[:r]) * row_bytes
     nself = input_split_sizes[r] * row_bytes
-    if total_out:
-        outb[:total_out].copy_(recv[:total_out])
     if nself:
-        outb[self_out:self_out + nself].copy_(inb[self_in:self_in + nself])
+        recv[self_out:self_out + nself].copy_(inb[self_in:self_in + nself])
+    if check_splits:
+        comm._check_output_splits(comm._counts_for(tuple(output_split_sizes), row_bytes, True))
+    res = recv[:total_out].view(input.dtype).view(-1, *input.shape[1:])
+    if output is None:
+        return res
+    if total_out:
+        output.view(torch.uint8).reshape(-1)[:total_out].copy_(recv[:total_out])
     return output
+
+
+class _AllToAllFast(torch.autograd.Function):
+    """all_to_all_fast with autograd: the backward is the reverse FAST
+    alltoallv of the output gradient (the transposed demand matrix D^T: the
+    split lists swap roles), as for all_to_all_single."""
+
+    @staticmethod
+    def forward(ctx, input, output_split_sizes, input_split_sizes, comm, bwd_comm):
+        ctx.splits = (list(output_split_sizes), list(input_split_sizes))
+        ctx.comm = bwd_comm or comm
+        out = torch.empty((sum(output_split_sizes),) + tuple(input.shape[1:]), dtype=input.dtype,
+                          device=input.device)
+        return all_to_all_fast(out, input, output_split_sizes, input_split_sizes, comm=comm)
+
+    @staticmethod
+    def backward(ctx, grad):
+        out_s, in_s = ctx.splits
+        g = grad.contiguous()
+        gin = torch.empty((sum(in_s),) + tuple(g.shape[1:]), dtype=g.dtype, device=g.device)
+        all_to_all_fast(gin, g, in_s, out_s, comm=ctx.comm)
+        return gin, None, None, None, None
+
+
+def all_to_all_fast_autograd(input: torch.Tensor, output_split_sizes: list[int],
+                             input_split_sizes: list[int], comm: FastComm,
+                             bwd_comm: FastComm | None = None) -> torch.Tensor:
+    """Differentiable all_to_all_fast (returns a new tensor; the backward runs
+    on `bwd_comm`, default `comm`)."""
+    return _AllToAllFast.apply(input, output_split_sizes, input_split_sizes, comm, bwd_comm)
 
 
 class GroupRank:
@@ -384,7 +517,8 @@ class GroupComm:
     def alltoallv(self, sends: list[torch.Tensor], D: torch.Tensor,
                   stream: torch.cuda.Stream | None = None,
                   self_bytes: torch.Tensor | None = None,
-                  send_rows: list | None = None) -> list[torch.Tensor]:
+                  send_rows: list | None = None,
+                  exec_events: tuple | None = None) -> list[torch.Tensor]:
         """D: [world, world] int64, zero diagonal.  self_bytes (optional,
         int64[world]): own segments kept in place in send_g and left as a
         gap in recv_g (all_to_all_single layout).  send_rows (optional, per
@@ -398,7 +532,7 @@ class GroupComm:
                     ctypes.c_void_p(row_src.data_ptr()), int(rb), row_src.numel()),
                     "fast_comm_set_send_rows")
             try:
-                return self.alltoallv(sends, D, stream, self_bytes)
+                return self.alltoallv(sends, D, stream, self_bytes, exec_events=exec_events)
             finally:
                 for r in range(self.world):
                     lib.fast_comm_set_send_rows(self._ptrs[r], None, None, 0, 0)
@@ -418,11 +552,24 @@ class GroupComm:
                                             ctypes.byref(self.plan.struct), sh),
                       "fast_plan_compile")
         sp = (ctypes.c_void_p * self.world)(*[s.data_ptr() for s in sends])
+        if exec_events is not None:
+            exec_events[0].record(stream or torch.cuda.current_stream())
         _lib.check_rc(lib.fast_exec_group(self._ptrs, self.world, ctypes.byref(self.plan.struct),
                                           sp, self.epoch, self.blocks, self.chunk,
                                           ctypes.c_void_p(self.timeline.data_ptr()), sh),
                       "fast_exec_group")
+        if exec_events is not None:
+            exec_events[1].record(stream or torch.cuda.current_stream())
         return self.recvs
+
+    def measured_timeline(self, rank: int) -> Timeline:
+        """Measured Timeline of `rank` in the last call (syncs)."""
+        st = self.timeline.view(self.world, TIMELINE_STRIDE)[rank].cpu().numpy()
+        return _timeline_from(st, self.plan.host_ops(), rank)
+
+    def measured_phases(self, rank: int) -> dict:
+        st = self.timeline.view(self.world, TIMELINE_STRIDE)[rank].cpu().numpy()
+        return phase_windows(st, _n_stages_of(self.plan.host_ops()))
 
     def check(self) -> None:
         lib = _lib.load()

@@ -4,7 +4,7 @@ alltoallv -> unpack, all on the device (BASELINE config 3).
     disp = MoEDispatch(comm, tokens_per_gpu=16384, row_bytes=8192)
     expert_in = disp.dispatch(tokens, seed=0)   # [recv rows, row_bytes] uint8
 
-Expert e lives on rank e (E = world).  The receive region of the executor is
+Rank r hosts experts [r*L, (r+1)*L) (E = L * world).  The receive region of the executor is
 laid out like all_to_all_single's output with a gap at the self slot; the
 unpack kernel copies the local segment into that gap, so the receive region
 IS the expert input (source-major, stable token order within a source).
@@ -36,24 +36,36 @@ def gating_thresholds(E: int, alpha: float = 0.8, hot: int = 0) -> tuple[np.ndar
 
 
 class MoEDispatch:
-    """Device buffers + the five kernels of one MoE dispatch (one rank)."""
+    """Device buffers + the kernels of one MoE dispatch (one rank).
+
+    num_experts E (default: the world size) must be a multiple of the world
+    W; rank r hosts experts [r*L, (r+1)*L), L = E / W.  The top-k expert ids
+    come from the caller's router (``dispatch(tokens, topk=...)``, int32
+    [T, k], k in 1/2/4/8) or, for benchmarks, from the deterministic
+    synthetic top-2 gate (``dispatch(tokens, seed=...)``).  The send layout
+    is expert-major (Megatron's permute order), so each destination rank
+    receives, per source, its experts' rows expert by expert."""
 
     def __init__(self, comm, tokens_per_gpu: int, row_bytes: int, k: int = 2,
-                 alpha: float = 0.8, fused_pack: bool = False):
+                 alpha: float = 0.8, fused_pack: bool = False, num_experts: int | None = None):
         if row_bytes % 16:
             raise ValidationError("row_bytes must be a multiple of 16")
-        if k != 2:
-            raise ValidationError("the synthetic gate is top-2")
+        if k not in (1, 2, 4, 8):
+            raise ValidationError("top-k must be 1, 2, 4 or 8")
         self.comm = comm
         self.T, self.row_bytes, self.k = tokens_per_gpu, row_bytes, k
-        self.E = comm.world
+        self.E = int(num_experts or comm.world)
+        if self.E % comm.world or self.E > 64:
+            raise ValidationError(f"num_experts {self.E} must be a multiple of the world size "
+                                  f"{comm.world} and <= 64")
+        self.L = self.E // comm.world
         dev = comm.device
         lib = _lib.load()
         self.topk = torch.empty(self.T * k, dtype=torch.int32, device=dev)
         self.pos = torch.empty(self.T * k, dtype=torch.int32, device=dev)
         self.counts = torch.empty(self.E, dtype=torch.int64, device=dev)
         self.seg_rows = torch.empty(self.E, dtype=torch.int64, device=dev)
-        self.demand_row = torch.empty(self.E, dtype=torch.int64, device=dev)
+        self.demand_row = torch.empty(comm.world, dtype=torch.int64, device=dev)
         self.ws = torch.empty(max(16, int(lib.fast_moe_route_workspace_bytes(self.T, k, self.E))),
                               dtype=torch.uint8, device=dev)
         # fused_pack: the executor reads token rows through row_src (4 B per
@@ -69,17 +81,34 @@ class MoEDispatch:
         self.thr = torch.from_numpy(thr.view(np.int64)).to(self.comm.device)
         self.thr2 = torch.from_numpy(np.ascontiguousarray(thr2).view(np.int64)).to(self.comm.device)
 
-    def route(self, seed: int, stream=None) -> None:
-        """gating + histogram/scan (the traffic-matrix builder, row of D)."""
+    def route(self, seed: int | None = None, stream=None,
+              topk: torch.Tensor | None = None) -> None:
+        """Top-k ids (the router's, or the synthetic gate's for `seed`) ->
+        histogram / scan: stable send rows, per-expert counts and this rank's
+        row of the demand matrix (the traffic-matrix builder)."""
         lib = _lib.load()
         sh = _stream_handle(stream)
         P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
-        _lib.check_rc(lib.fast_moe_gate(self.T, ctypes.c_uint64(seed * 1000 + self.comm.rank),
-                                        self.E, P(self.thr), P(self.thr2), P(self.topk), sh),
-                      "fast_moe_gate")
-        _lib.check_rc(lib.fast_moe_route(P(self.topk), self.T, self.k, self.E, self.row_bytes,
-                                         P(self.pos), P(self.counts), P(self.seg_rows),
-                                         P(self.demand_row), P(self.ws), sh), "fast_moe_route")
+        if topk is not None:
+            if (topk.dtype != torch.int32 or not topk.is_cuda
+                    or topk.numel() != self.T * self.k):
+                raise ValidationError(f"topk must be a cuda int32 tensor [{self.T}, {self.k}]")
+            self.topk = topk.contiguous().view(-1)
+        else:
+            if seed is None:
+                raise ValidationError("route needs the router's topk or a gate seed")
+            if self.k != 2:
+                raise ValidationError("the synthetic gate is top-2; pass the router's topk")
+            if self.topk.numel() != self.T * self.k or self.topk.data_ptr() == 0:
+                self.topk = torch.empty(self.T * self.k, dtype=torch.int32,
+                                        device=self.comm.device)
+            _lib.check_rc(lib.fast_moe_gate(self.T, ctypes.c_uint64(seed * 1000 + self.comm.rank),
+                                            self.E, P(self.thr), P(self.thr2), P(self.topk), sh),
+                          "fast_moe_gate")
+        _lib.check_rc(lib.fast_moe_route_ex(P(self.topk), self.T, self.k, self.E, self.L,
+                                            self.row_bytes, P(self.pos), P(self.counts),
+                                            P(self.seg_rows), P(self.demand_row), P(self.ws), sh),
+                      "fast_moe_route_ex")
 
     def pack(self, tokens: torch.Tensor, stream=None) -> None:
         lib = _lib.load()
@@ -129,10 +158,12 @@ class MoEDispatch:
                                                _stream_handle(stream)), "fast_moe_unpack_self")
         return recv
 
-    def dispatch(self, tokens: torch.Tensor, seed: int, stream=None) -> torch.Tensor:
+    def dispatch(self, tokens: torch.Tensor, seed: int | None = None, stream=None,
+                 topk: torch.Tensor | None = None) -> torch.Tensor:
         """Full dispatch; returns the receive region (expert input rows,
-        source-major; the row count is counts summed over sources)."""
-        self.route(seed, stream)
+        source-major; per source this rank's experts in order; the row count
+        is this rank's experts' counts summed over sources)."""
+        self.route(seed, stream, topk)
         if self.fused_pack:
             self.rowmap(stream, tokens)
             self.comm.alltoallv(self._tokens, self.demand_row, stream=stream,
@@ -140,7 +171,11 @@ class MoEDispatch:
         else:
             self.pack(tokens, stream)
             self.comm.alltoallv(self.send, self.demand_row, stream=stream)
-        self.remember_forward(self.comm.demand(), self.comm.self_sizes())
+        # the demand matrix lands on `stream`: snapshot it there (not on the
+        # current stream, which may run ahead of a side stream)
+        s = stream or torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            self.remember_forward(self.comm.demand(), self.comm.self_sizes())
         return self.unpack(stream)
 
     def remember_forward(self, D: torch.Tensor, self_sizes: torch.Tensor) -> None:
@@ -150,6 +185,17 @@ class MoEDispatch:
         self.Dfwd = D.clone()
         self.comb_counts = D[:, r].clone()
         self.comb_counts[r] = self_sizes[r]
+
+    def tokens_per_expert(self) -> torch.Tensor:
+        """[world, L] rows this rank received per (source, local expert) in
+        the last dispatch (Megatron's num_global_tokens_per_expert slice).
+        Uses the process group (FastComm only)."""
+        import torch.distributed as dist
+
+        allc = torch.empty(self.comm.world, self.E, dtype=torch.int64, device=self.comm.device)
+        dist.all_gather_into_tensor(allc, self.counts)
+        r, L = self.comm.rank, self.L
+        return allc[:, r * L:(r + 1) * L]
 
     def combine_rows(self, comb_recv: torch.Tensor, expert_out: torch.Tensor,
                      weights: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
@@ -161,11 +207,12 @@ class MoEDispatch:
             raise ValidationError("weights must be float32 [T, k]")
         if out.dtype != torch.bfloat16 or out.numel() * 2 != self.T * self.row_bytes:
             raise ValidationError("out must be bf16 [T, row_bytes/2]")
-        _lib.check_rc(lib.fast_moe_combine(P(comb_recv), P(expert_out), P(self.Dfwd),
-                                           self.comm.world, self.comm.rank, self.T, self.k,
-                                           self.row_bytes, P(self.topk), P(self.pos), P(self.ws),
-                                           self.E, P(self.seg_rows), P(weights.contiguous()),
-                                           P(out), _stream_handle(stream)), "fast_moe_combine")
+        _lib.check_rc(lib.fast_moe_combine_ex(P(comb_recv), P(expert_out), P(self.Dfwd),
+                                              self.comm.world, self.comm.rank, self.T, self.k,
+                                              self.row_bytes, P(self.topk), P(self.pos),
+                                              P(self.ws), self.E, self.L, P(self.seg_rows),
+                                              P(weights.contiguous()), P(out),
+                                              _stream_handle(stream)), "fast_moe_combine_ex")
         return out
 
     def combine(self, expert_out: torch.Tensor, weights: torch.Tensor, out: torch.Tensor,

@@ -88,6 +88,30 @@ def main() -> int:
         if not torch.equal(y_fast.cpu().view(torch.int16), y_ref.cpu().view(torch.int16)):
             print(f"[rank {rank}] all_to_all_fast != all_to_all_single (n={n}, m={m})", flush=True)
             ok = False
+        # zero-copy result (a view of the receive region) and the split check
+        y0 = all_to_all_fast(None, x, splits[:, rank].tolist(), splits[rank].tolist(), comm=comm)
+        torch.cuda.synchronize()
+        comm.check()
+        if not torch.equal(y0.cpu().view(torch.int16), y_ref.cpu().view(torch.int16)):
+            print(f"[rank {rank}] zero-copy all_to_all_fast mismatch (n={n}, m={m})", flush=True)
+            ok = False
+        # autograd: the backward is the reverse FAST alltoallv (splits swapped)
+        from paper_2505_09764_b200.executor import all_to_all_fast_autograd
+
+        xf = xs[rank].float().cuda().requires_grad_(True)
+        yf = all_to_all_fast_autograd(xf, splits[:, rank].tolist(), splits[rank].tolist(), comm)
+        wg = [torch.randn(int(splits[:, h].sum()), 4096,
+                          generator=torch.Generator().manual_seed(900 + h)) for h in range(world)]
+        (yf * wg[rank].cuda()).sum().backward()
+        torch.cuda.synchronize()
+        comm.check()
+        # d loss / d x_rank: rows of wg[h] that rank's rows landed on, h-major
+        want_g = torch.cat([wg[h][int(splits[:rank, h].sum()):int(splits[:rank + 1, h].sum())]
+                            for h in range(world)])
+        if not torch.equal(yf.detach().cpu(), y_ref.cpu().float()) or \
+                not torch.equal(xf.grad.cpu(), want_g):
+            print(f"[rank {rank}] all_to_all_fast autograd mismatch (n={n}, m={m})", flush=True)
+            ok = False
         # MoE dispatch (config 3 shape, scaled): expert inputs vs the oracle
         from oracle import moe as moe_oracle
         from paper_2505_09764_b200.moe import MoEDispatch, gating_thresholds
@@ -138,6 +162,31 @@ def main() -> int:
             gotc = out.cpu().view(torch.int16).numpy().view(np.uint16)
             if not np.array_equal(gotc, wantc):
                 print(f"[rank {rank}] MoE combine mismatch (n={n}, m={m})", flush=True)
+                ok = False
+        # router-provided top-k, E = 2 * world experts (2 per rank), k = 2
+        E2, L2 = 2 * world, 2
+        rdisp = MoEDispatch(mcomm, T, RB, num_experts=E2)
+        rtk = [np.random.default_rng(4000 + s_).integers(0, E2, (T, 2)).astype(np.int32)
+               for s_ in range(world)]
+        rrecv = rdisp.dispatch(torch.from_numpy(toks[rank]).cuda(),
+                               topk=torch.from_numpy(rtk[rank]).cuda())
+        torch.cuda.synchronize()
+        mcomm.check()
+        rwant = moe_oracle.expert_inputs(toks, rtk, E2, L2)[rank]
+        if not np.array_equal(rrecv[: rwant.size].cpu().numpy().reshape(-1, RB), rwant):
+            print(f"[rank {rank}] router-topk MoE expert input mismatch (n={n}, m={m})", flush=True)
+            ok = False
+        rn = rwant.size
+        rexp = torch.zeros(2 * T * RB * 3, dtype=torch.uint8, device="cuda")
+        rexp[:rn].copy_((rrecv[:rn].view(torch.bfloat16) * (2.0 ** rank)).view(torch.uint8))
+        rout = torch.empty(T, RB // 2, dtype=torch.bfloat16, device="cuda")
+        rdisp.combine(rexp, torch.from_numpy(wts[rank]).cuda(), rout)
+        torch.cuda.synchronize()
+        mcomm.check()
+        if finite:
+            wantr = moe_oracle.combine(toks16, rtk, wts, lambda e: 2.0 ** (e // L2))[rank]
+            if not np.array_equal(rout.cpu().view(torch.int16).numpy().view(np.uint16), wantr):
+                print(f"[rank {rank}] router-topk MoE combine mismatch (n={n}, m={m})", flush=True)
                 ok = False
         mcomm.close()
         comm.close()

@@ -38,16 +38,28 @@ class _GlooComm:
     """Stand-in transport with FastComm's alltoallv contract (receive layout
     of all_to_all_single with a gap at the self slot)."""
 
+    recv_bytes = 1 << 30
+
     def __init__(self):
         self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.split_errors = 0
+
+    def _counts_for(self, splits, row_bytes, out=False):
+        return torch.tensor([int(x) * int(row_bytes) for x in splits], dtype=torch.int64)
+
+    def _check_output_splits(self, out_bytes):
+        col = self.D[:, self.rank]
+        self.split_errors += int((col != out_bytes).any())
 
     def alltoallv(self, send: torch.Tensor, counts: torch.Tensor) -> torch.Tensor:
         rows = [torch.zeros(self.world, dtype=torch.int64) for _ in range(self.world)]
         dist.all_gather(rows, counts.to(torch.int64))
         D = torch.stack(rows)
+        self.D = D
         out_splits = D[:, self.rank].tolist()
-        recv = torch.empty(int(sum(out_splits)), dtype=torch.uint8)
-        dist.all_to_all_single(recv, send[: int(counts.sum())], out_splits, counts.tolist())
+        recv = torch.zeros(int(sum(out_splits)) + 4096, dtype=torch.uint8)  # region slack
+        dist.all_to_all_single(recv[: int(sum(out_splits))], send[: int(counts.sum())], out_splits,
+                               counts.tolist())
         lo = int(sum(out_splits[: self.rank]))
         recv[lo:lo + out_splits[self.rank]] = 0  # the self slot is a gap
         return recv
@@ -118,9 +130,26 @@ def _worker(rank: int, port: int, errq, WORLD: int, n: int, m: int):
         x = torch.arange(int(splits[rank].sum()) * 6, dtype=torch.int32).reshape(-1, 6) + 1000 * rank
         y_fast = torch.zeros(int(splits[:, rank].sum()), 6, dtype=torch.int32)
         y_ref = torch.zeros_like(y_fast)
-        all_to_all_fast(y_fast, x, splits[:, rank].tolist(), splits[rank].tolist(), comm=_GlooComm())
+        gc = _GlooComm()
+        all_to_all_fast(y_fast, x, splits[:, rank].tolist(), splits[rank].tolist(), comm=gc)
         dist.all_to_all_single(y_ref, x, splits[:, rank].tolist(), splits[rank].tolist())
         assert torch.equal(y_fast, y_ref)
+        y0 = all_to_all_fast(None, x, splits[:, rank].tolist(), splits[rank].tolist(), comm=gc)
+        assert torch.equal(y0, y_ref) and gc.split_errors == 0  # zero-copy view
+        wrong = splits[:, rank].copy()
+        wrong[(rank + 1) % G] += 1
+        all_to_all_fast(None, x, wrong.tolist(), splits[rank].tolist(), comm=gc)
+        assert gc.split_errors == 1  # output splits checked against the gathered counts
+        # 5. autograd: backward is the reverse alltoallv (splits swapped)
+        from paper_2505_09764_b200.executor import all_to_all_fast_autograd
+
+        xf = (x.to(torch.float64) / 7).requires_grad_(True)
+        yf = all_to_all_fast_autograd(xf, splits[:, rank].tolist(), splits[rank].tolist(), gc)
+        wgt = torch.arange(yf.numel(), dtype=torch.float64).reshape(yf.shape) + rank
+        (yf * wgt).sum().backward()
+        want = torch.zeros_like(xf)
+        dist.all_to_all_single(want, wgt, splits[rank].tolist(), splits[:, rank].tolist())
+        assert torch.equal(xf.grad, want)
         dist.destroy_process_group()
     except Exception as exc:  # pragma: no cover - reported by the parent
         import traceback

@@ -208,3 +208,46 @@ def test_group_exec_wide_partitions(n, m):
     _check(comm, D)
     _check(comm, workloads.gen_adversarial(Topology(n, m), 1_000_003).sizes)
     comm.close()
+
+
+@pytest.mark.parametrize("n,m", [(2, 4), (4, 2)])
+def test_group_exec_measured_timeline(n, m):
+    """The measured Timeline (the reference's phase breakdown,
+    simulate.py:38-55) is filled from device stamps: every phase that has
+    chunks has a non-empty window, windows lie inside [0, total], the stage
+    sends follow the plan's phase order (balance before the stages that
+    forward balanced-in bytes), and the slowest rank's total matches the CUDA
+    event time of the exec kernel within 5 %."""
+    from paper_2505_09764_b200.executor import PH_BALANCE, PH_REDIST, STAGE_INTRA
+
+    D = workloads.zipf_sizes(0, n * m, 1.2, 1 << 28)
+    comm = _comm_for(n, m, D, blocks=16, chunk=1 << 20)
+    sends = _sends(D)
+    Dt = torch.from_numpy(D).cuda()
+    comm.alltoallv(sends, Dt)  # warm-up
+    ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    comm.alltoallv(sends, Dt, exec_events=ev)
+    torch.cuda.synchronize()
+    comm.check()
+    ops = comm.plan.host_ops()
+    totals = []
+    for r in range(n * m):
+        tl = comm.measured_timeline(r)
+        ph = comm.measured_phases(r)
+        mine = ops[ops["exec_rank"] == r]
+        assert tl.total > 0 and ph["barrier"] >= 0
+        has_bal = bool((mine["phase"] == PH_BALANCE).any())
+        has_intra = bool((mine["stage"] == STAGE_INTRA).any())
+        assert (tl.t_balance > 0) == has_bal and (tl.t_intra_a2a > 0) == has_intra, r
+        for k in range(len(tl.scale_out)):
+            sel = mine[mine["stage"] == k]
+            assert (tl.scale_out[k] > 0) == bool((sel["phase"] != PH_REDIST).any()), (r, k)
+            assert (tl.redistribution[k] > 0) == bool((sel["phase"] == PH_REDIST).any()), (r, k)
+        wins = [w for w in [ph["balance"], ph["intra"], *ph["scale_out"], *ph["redistribution"]]
+                if w is not None]
+        for a, b in wins:
+            assert ph["barrier"] <= a <= b <= tl.total + 1e-6, (r, a, b, tl.total)
+        totals.append(tl.total)
+    ev_s = ev[0].elapsed_time(ev[1]) * 1e-3
+    assert abs(max(totals) - ev_s) <= 0.05 * ev_s, (max(totals), ev_s)
+    comm.close()

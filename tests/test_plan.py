@@ -101,6 +101,7 @@ def check_instance(D: np.ndarray, n: int, m: int, chunk: int = 4096):
         e, d = int(o["exec_rank"]), int(o["dst_rank"])
         if e // m == d // m:
             assert o["phase"] == PH_DIRECT and o["dst_buf"] == BUF_RECV  # intra tile
+            assert o["stage"] == 255  # FAST_STAGE_INTRA
             continue
         assert e % m == d % m, "stage traffic must go lane p -> proxy p"
         per_stage[(int(o["stage"]), e // m, d // m)] += int(o["len"])
