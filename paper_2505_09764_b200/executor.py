@@ -137,14 +137,16 @@ def _n_stages_of(ops: np.ndarray | None) -> int:
 def _timeline_from(stamps: np.ndarray, ops: np.ndarray | None, rank: int) -> Timeline:
     """Measured Timeline of one rank (the reference's phase breakdown,
     simulate.py:38-55): each phase's duration is its window on this rank
-    (first chunk start to last chunk end); total = exec start -> every byte
-    addressed to this rank has landed."""
+    (first chunk start to last chunk end); total = exec start -> this rank
+    has sent its last chunk and every byte addressed to it has landed."""
     w = phase_windows(stamps, _n_stages_of(ops))
     dur = lambda x: 0.0 if x is None else max(0.0, x[1] - x[0])  # noqa: E731
+    ends = [x[1] for x in [w["balance"], w["intra"], *w["scale_out"], *w["redistribution"]]
+            if x is not None]
     return Timeline(t_balance=dur(w["balance"]), t_intra_a2a=dur(w["intra"]),
                     scale_out=tuple(dur(x) for x in w["scale_out"]),
                     redistribution=tuple(dur(x) for x in w["redistribution"]),
-                    total=max(0.0, w["recv_done"]))
+                    total=max([0.0, w["recv_done"], *ends]))
 
 
 class FastComm:
