@@ -64,10 +64,29 @@ __device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
 __device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// Protocol fuzzing (-DFAST_EXEC_FUZZ, test builds only): a pseudo-random
+// 0..4 us sleep before every signal and every wait, so the flag protocol is
+// exercised under arbitrary interleavings of producers and consumers.
+#ifdef FAST_EXEC_FUZZ
+__device__ __forceinline__ void fuzz_delay() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  uint32_t h = (uint32_t)(t ^ (t >> 17)) * 0x9E3779B1u ^ (blockIdx.x * 0x85EBCA6Bu) ^
+               (threadIdx.x * 0xC2B2AE35u) ^ (blockIdx.y * 0x27D4EB2Fu);
+  h ^= h >> 15;
+  if (h & 1) __nanosleep(h % 4096);
+}
+#define FAST_FUZZ() fuzz_delay()
+#else
+#define FAST_FUZZ()
+#endif
+
 __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  FAST_FUZZ();
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void red_release_sys_add(uint64_t* p, uint64_t v) {
+  FAST_FUZZ();
   asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -80,6 +99,7 @@ __device__ __forceinline__ uint64_t globaltimer() {
 // exponentially (to 512 ns) so that many waiting CTAs do not flood one L2
 // line while the CTA they wait for is working.
 __device__ bool wait_geq(const uint64_t* p, uint64_t target, bool sys) {
+  FAST_FUZZ();
   const uint64_t t0 = globaltimer();
   unsigned sleep_ns = 32;
   int spins = 0;
