@@ -143,6 +143,7 @@ struct ExecArgs {
   const uint8_t* rows_bases[kMaxRanks];  // group mode: per local rank slot
   const int32_t* row_srcs[kMaxRanks];
   int64_t send_cap;  // bytes readable from the send side (-1: unchecked)
+  int64_t recv_cap, staging_cap;  // region sizes of every rank's block
 };
 
 __device__ __forceinline__ uint64_t* ctr(uint8_t* base, int idx) {
@@ -612,13 +613,23 @@ __global__ void __launch_bounds__(kExecThreads) exec_kernel(ExecArgs a, FusedArg
   if (tid < 3) s_red[tid] = 0ull;
   __syncthreads();
   const int nops = (*a.plan_status == FAST_OK) ? *a.n_ops : 0;
-  // send-side bounds: the counts must fit the caller's send buffer
-  if (a.send_cap >= 0) {
+  // bounds of every op this rank executes (defence in depth: the plan
+  // compile already sizes everything): the send side against the caller's
+  // send buffer, the destination / staging ranges against the regions, the
+  // flag slots against the slot table.  Any violation: nothing is copied.
+  {
     bool over = false;
     for (int i = tid; i < nops; i += blockDim.x) {
       const fast_op o = a.ops[i];
-      over |= o.exec_rank == a.rank && o.src_buf == FAST_BUF_SEND &&
-              o.src_off + o.len > a.send_cap;
+      if (o.exec_rank != a.rank) continue;
+      const int64_t dcap = o.dst_buf == FAST_BUF_RECV ? a.recv_cap : a.staging_cap;
+      over |= o.len < 0 || o.src_off < 0 || o.dst_off < 0 || o.dst_off + o.len > dcap;
+      over |= o.dst_rank < 0 || o.dst_rank >= a.world;
+      if (o.src_buf == FAST_BUF_SEND) over |= a.send_cap >= 0 && o.src_off + o.len > a.send_cap;
+      else over |= o.src_off + o.len > a.staging_cap;
+      if (o.sig_slot >= 0) over |= o.sig_slot + nchunks(o.len, a.chunk) > FAST_MAX_SLOTS;
+      if (o.wait_slot >= 0)
+        over |= o.wait_slot + (o.wait_off + o.len + a.chunk - 1) / a.chunk > FAST_MAX_SLOTS;
     }
     if (__syncthreads_or(over)) {
       if (tid == 0) s_fail = 2;  // validation: nothing is copied
@@ -997,6 +1008,8 @@ static int exec_launch(fast_comm* c, const fast_plan* plan, const void* send, in
   a.skip_barrier = skip_barrier;
   set_rowmap(a, c);
   a.send_cap = c->send_cap;
+  a.recv_cap = c->recv_bytes;
+  a.staging_cap = c->staging_bytes;
   FusedArgs f;
   memset(&f, 0, sizeof(f));
   exec_kernel<false><<<blocks, kExecThreads, 0, (cudaStream_t)stream>>>(a, f);
@@ -1054,6 +1067,8 @@ int fast_exec_group(fast_comm* const* comms, int world, const fast_plan* plan,
   a.rank = 0;
   a.world = world;
   a.send_cap = -1;
+  a.recv_cap = comms[0]->recv_bytes;
+  a.staging_cap = comms[0]->staging_bytes;
   FusedArgs f;
   memset(&f, 0, sizeof(f));
   void* args[] = {&a, &f};
@@ -1118,6 +1133,8 @@ static int launch_fused(fast_comm* c, const void* send, const int64_t* counts, i
   a.skip_barrier = 1;  // the in-kernel demand all-gather synchronises the ranks
   set_rowmap(a, c);
   a.send_cap = c->send_cap;
+  a.recv_cap = c->recv_bytes;
+  a.staging_cap = c->staging_bytes;
   FusedArgs f;
   memset(&f, 0, sizeof(f));
   f.counts = counts;
