@@ -306,6 +306,83 @@ __device__ __forceinline__ void load_row64(const uint32_t* src, uint64_t& r0, ui
   "st.shared.u16 [pa], t;\n\t"                                        \
   "add.u32 pa, pa, 2;\n\t"
 
+// v2 step (default): select the first non-empty word (and its row
+// base) with predicates first, then ONE bfind on it -- one FLO per step
+// instead of four, and the seen update touches only the selected word.
+#define FAST_DFS_STEP4_V2(R0, R1, R2, R3, N0, N1, N2, N3)              \
+  "and.b32 x0, " R1 ", ns0;\n\t"                                      \
+  "and.b32 x1, " R0 ", ns1;\n\t"                                      \
+  "and.b32 x2, " R3 ", ns2;\n\t"                                      \
+  "and.b32 x3, " R2 ", ns3;\n\t"                                      \
+  "setp.ne.u32 p0, x0, 0;\n\t"                                        \
+  "setp.ne.u32 p2, x2, 0;\n\t"                                        \
+  "or.b32 t, x0, x1;\n\t"                                             \
+  "setp.ne.u32 p01, t, 0;\n\t"                                        \
+  "selp.b32 a0, x0, x1, p0;\n\t"                                      \
+  "selp.b32 a2, x2, x3, p2;\n\t"                                      \
+  "selp.b32 a1, bb0, bb1, p0;\n\t"                                    \
+  "selp.b32 a3, bb2, bb3, p2;\n\t"                                    \
+  "selp.b32 a0, a0, a2, p01;\n\t"                                     \
+  "selp.b32 a1, a1, a3, p01;\n\t"                                     \
+  "bfind.shiftamt.u32 z0, a0;\n\t"                                    \
+  "mad.lo.u32 ad, z0, 16, a1;\n\t"                                    \
+  "ld.shared.v4.u32 {" N0 ", " N1 ", " N2 ", " N3 "}, [ad];\n\t"     \
+  "setp.eq.u32 pn, a0, 0;\n\t"                                        \
+  "@pn bra.uni FDFS_BACK;\n\t"                                        \
+  "setp.ne.and.u32 p1, x1, 0, !p0;\n\t"                               \
+  "setp.ne.and.u32 p3, x2, 0, !p01;\n\t"                              \
+  "or.b32 u, t, x2;\n\t"                                              \
+  "setp.eq.u32 pz, u, 0;\n\t"                                         \
+  "shr.u32 z0, hb, z0;\n\t"                                           \
+  "not.b32 z0, z0;\n\t"                                               \
+  "@p0 and.b32 ns0, ns0, z0;\n\t"                                     \
+  "@p1 and.b32 ns1, ns1, z0;\n\t"                                     \
+  "@p3 and.b32 ns2, ns2, z0;\n\t"                                     \
+  "@pz and.b32 ns3, ns3, z0;\n\t"                                     \
+  "sub.u32 t, ad, bb0;\n\t"                                           \
+  "st.shared.u16 [pa], t;\n\t"                                        \
+  "add.u32 pa, pa, 2;\n\t"
+
+// v3 step (-DFAST_DFS_V3): per-half select, two bfinds in parallel, the
+// address selected last (one dependent op less than v2 on the chain).
+#define FAST_DFS_STEP4_V3(R0, R1, R2, R3, N0, N1, N2, N3)              \
+  "and.b32 x0, " R1 ", ns0;\n\t"                                      \
+  "and.b32 x1, " R0 ", ns1;\n\t"                                      \
+  "and.b32 x2, " R3 ", ns2;\n\t"                                      \
+  "and.b32 x3, " R2 ", ns3;\n\t"                                      \
+  "setp.ne.u32 p0, x0, 0;\n\t"                                        \
+  "setp.ne.u32 p2, x2, 0;\n\t"                                        \
+  "or.b32 t, x0, x1;\n\t"                                             \
+  "setp.ne.u32 p01, t, 0;\n\t"                                        \
+  "selp.b32 a0, x0, x1, p0;\n\t"                                      \
+  "selp.b32 a2, x2, x3, p2;\n\t"                                      \
+  "selp.b32 a1, bb0, bb1, p0;\n\t"                                    \
+  "selp.b32 a3, bb2, bb3, p2;\n\t"                                    \
+  "bfind.shiftamt.u32 z0, a0;\n\t"                                    \
+  "bfind.shiftamt.u32 z2, a2;\n\t"                                    \
+  "mad.lo.u32 a1, z0, 16, a1;\n\t"                                    \
+  "mad.lo.u32 a3, z2, 16, a3;\n\t"                                    \
+  "selp.b32 ad, a1, a3, p01;\n\t"                                     \
+  "ld.shared.v4.u32 {" N0 ", " N1 ", " N2 ", " N3 "}, [ad];\n\t"     \
+  "or.b32 u, t, x2;\n\t"                                              \
+  "or.b32 u, u, x3;\n\t"                                              \
+  "setp.eq.u32 pn, u, 0;\n\t"                                         \
+  "@pn bra.uni FDFS_BACK;\n\t"                                        \
+  "setp.ne.and.u32 p1, x1, 0, !p0;\n\t"                               \
+  "setp.ne.and.u32 p3, x2, 0, !p01;\n\t"                              \
+  "or.b32 u, t, x2;\n\t"                                              \
+  "setp.eq.u32 pz, u, 0;\n\t"                                         \
+  "selp.b32 z0, z0, z2, p01;\n\t"                                     \
+  "shr.u32 z0, hb, z0;\n\t"                                           \
+  "not.b32 z0, z0;\n\t"                                               \
+  "@p0 and.b32 ns0, ns0, z0;\n\t"                                     \
+  "@p1 and.b32 ns1, ns1, z0;\n\t"                                     \
+  "@p3 and.b32 ns2, ns2, z0;\n\t"                                     \
+  "@pz and.b32 ns3, ns3, z0;\n\t"                                     \
+  "sub.u32 t, ad, bb0;\n\t"                                           \
+  "st.shared.u16 [pa], t;\n\t"                                        \
+  "add.u32 pa, pa, 2;\n\t"
+
 #define FAST_DFS_STEP2(R0, R1, N0, N1)                                 \
   "and.b32 x0, " R1 ", ns0;\n\t"                                      \
   "and.b32 x1, " R0 ", ns1;\n\t"                                      \
@@ -376,7 +453,7 @@ __device__ __forceinline__ int dfs_search_body(const uint32_t root_a, const uint
   if constexpr (NWP == 4) {
     asm volatile(
         "{\n\t"
-        ".reg .pred p0, p2, p01, pn, pz;\n\t"
+        ".reg .pred p0, p1, p2, p3, p01, pn, pz;\n\t"
         ".reg .b32 r0, r1, r2, r3, n0, n1, n2, n3, ns0, ns1, ns2, ns3;\n\t"
         ".reg .b32 x0, x1, x2, x3, z0, z1, z2, z3, a0, a1, a2, a3;\n\t"
         ".reg .b32 ad, t, u, pa, hb, bb0, bb1, bb2, bb3;\n\t"
@@ -392,8 +469,16 @@ __device__ __forceinline__ int dfs_search_body(const uint32_t root_a, const uint
         "add.u32 bb3, %4, 1536;\n\t"
         "ld.shared.v4.u32 {r0, r1, r2, r3}, [%1];\n\t"
         "FDFS_LOOP:\n\t"
+#if defined(FAST_DFS_V1)
         FAST_DFS_STEP4("r0", "r1", "r2", "r3", "n0", "n1", "n2", "n3")
         FAST_DFS_STEP4("n0", "n1", "n2", "n3", "r0", "r1", "r2", "r3")
+#elif defined(FAST_DFS_V3)
+        FAST_DFS_STEP4_V3("r0", "r1", "r2", "r3", "n0", "n1", "n2", "n3")
+        FAST_DFS_STEP4_V3("n0", "n1", "n2", "n3", "r0", "r1", "r2", "r3")
+#else  // v2: measured fastest for the batched (contended) case
+        FAST_DFS_STEP4_V2("r0", "r1", "r2", "r3", "n0", "n1", "n2", "n3")
+        FAST_DFS_STEP4_V2("n0", "n1", "n2", "n3", "r0", "r1", "r2", "r3")
+#endif
         "bra.uni FDFS_LOOP;\n\t"
         FAST_DFS_BACK("4", "ld.shared.v4.u32 {r0, r1, r2, r3}, [ad];\n\t")
         "}"
