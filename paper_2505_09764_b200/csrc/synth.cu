@@ -190,56 +190,88 @@ __global__ void __launch_bounds__(kDecWarps * 32)
 }
 
 // ---------------------------------------------------------------------------
-// sort_stages_ascending: bitonic sort of (weight, src0<<24|dst0<<16|idx).
-__global__ void __launch_bounds__(1024)
-    sort_kernel(const int n, fast_sched_bufs out) {
-  extern __shared__ __align__(16) char ssm[];
-  const int b = blockIdx.x;
-  const int K = stage_cap(n);
+// sort_stages_ascending (birkhoff.py:255-266): sort of the kept stages by
+// (weight, src0, dst0, raw index) -- the raw index makes it equal to
+// Python's stable sort.  Bitonic network in the "flip" form (every merge
+// ascending, the first step of each merge compares i with its mirror), which
+// sorts any count by skipping partners past the end: no padding.
+//
+// Common case: weight < 2^36, so (weight, src0, dst0, idx) packs into ONE
+// u64 (36 + 7 + 7 + 14 bits) and the keys live in shared memory: 8 bytes per
+// stage (129 KiB at n = 128), small enough to co-reside with the latency-
+// bound decomposition CTAs of concurrent batches.  Wider weights: the same
+// network runs on the (weight, tie) pairs in the global workspace.
+template <typename CMPX>
+__device__ __forceinline__ void bitonic_flip(const int cnt, CMPX cmpx) {
   int P = 1;
-  while (P < K) P <<= 1;
-  uint64_t* kw = (uint64_t*)ssm;
-  uint32_t* kt = (uint32_t*)(ssm + (size_t)P * 8);
-  if (out.status[b] != FAST_OK) return;
-  const int kept = out.n_stages[b];
-  if (kept <= 0) return;
-  int Q = 1;
-  while (Q < kept) Q <<= 1;
-  const int64_t* work =
-      (const int64_t*)((const char*)out.workspace + (size_t)b * dec_ws_bytes_per_matrix(n));
-  const uint64_t* key_w = (const uint64_t*)(work + (size_t)n * n);
-  const uint32_t* key_t = (const uint32_t*)(key_w + K);
-  for (int i = threadIdx.x; i < Q; i += blockDim.x) {
-    if (i < kept) {
-      kw[i] = key_w[i];
-      kt[i] = key_t[i];
-    } else {
-      kw[i] = ~0ull;
-      kt[i] = ~0u;
+  while (P < cnt) P <<= 1;
+  for (int kk = 2; kk <= P; kk <<= 1) {
+    const int half = kk >> 1;
+    for (int x = threadIdx.x; x < P / 2; x += blockDim.x) {
+      const int blk = x / half, o = x - blk * half;
+      const int i = blk * kk + o, j = blk * kk + kk - 1 - o;
+      if (j < cnt) cmpx(i, j);
     }
-  }
-  __syncthreads();
-  for (int kk = 2; kk <= Q; kk <<= 1) {
-    for (int j = kk >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < Q; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const bool asc = (i & kk) == 0;
-          const uint64_t wa = kw[i], wb = kw[ixj];
-          const uint32_t ta = kt[i], tb = kt[ixj];
-          const bool gt = wa > wb || (wa == wb && ta > tb);
-          if (gt == asc) {
-            kw[i] = wb; kw[ixj] = wa;
-            kt[i] = tb; kt[ixj] = ta;
-          }
-        }
+    __syncthreads();
+    for (int h = half >> 1; h > 0; h >>= 1) {
+      for (int x = threadIdx.x; x < P / 2; x += blockDim.x) {
+        const int blk = x / h, o = x - blk * h;
+        const int i = blk * 2 * h + o, j = i + h;
+        if (j < cnt) cmpx(i, j);
       }
       __syncthreads();
     }
   }
-  int32_t* ord = out.stage_order + (int64_t)b * K;
-  for (int i = threadIdx.x; i < kept; i += blockDim.x) ord[i] = (int32_t)(kt[i] & 0xffffu);
 }
+
+constexpr int kSortThreads = 1024;
+__global__ void __launch_bounds__(kSortThreads)
+    sort_kernel(const int n, fast_sched_bufs out) {
+  extern __shared__ __align__(16) unsigned long long sk[];
+  __shared__ unsigned long long s_max;
+  const int b = blockIdx.x;
+  const int K = stage_cap(n);
+  if (out.status[b] != FAST_OK) return;
+  const int kept = out.n_stages[b];
+  if (kept <= 0) return;
+  uint64_t* work = (uint64_t*)((char*)out.workspace + (size_t)b * dec_ws_bytes_per_matrix(n));
+  uint64_t* key_w = work + (size_t)n * n;
+  uint32_t* key_t = (uint32_t*)(key_w + K);
+  if (threadIdx.x == 0) s_max = 0;
+  __syncthreads();
+  unsigned long long mx = 0;
+  for (int i = threadIdx.x; i < kept; i += blockDim.x) mx = key_w[i] > mx ? key_w[i] : mx;
+  atomicMax(&s_max, mx);
+  __syncthreads();
+  int32_t* ord = out.stage_order + (int64_t)b * K;
+  if (s_max < (1ull << 36)) {
+    for (int i = threadIdx.x; i < kept; i += blockDim.x) {
+      const uint32_t t = key_t[i];  // src0 << 24 | dst0 << 16 | raw index
+      sk[i] = (key_w[i] << 28) | ((unsigned long long)((t >> 24) & 127) << 21) |
+              ((unsigned long long)((t >> 16) & 127) << 14) | (t & 0x3fffu);
+    }
+    __syncthreads();
+    bitonic_flip(kept, [&](int i, int j) {
+      const unsigned long long a = sk[i], c = sk[j];
+      if (a > c) { sk[i] = c; sk[j] = a; }
+    });
+    for (int i = threadIdx.x; i < kept; i += blockDim.x) ord[i] = (int32_t)(sk[i] & 0x3fffu);
+  } else {
+    volatile uint64_t* vw = key_w;
+    volatile uint32_t* vt = key_t;
+    bitonic_flip(kept, [&](int i, int j) {
+      const uint64_t wa = vw[i], wb = vw[j];
+      const uint32_t ta = vt[i], tb = vt[j];
+      if (wa > wb || (wa == wb && ta > tb)) {
+        vw[i] = wb; vw[j] = wa;
+        vt[i] = tb; vt[j] = ta;
+      }
+    });
+    for (int i = threadIdx.x; i < kept; i += blockDim.x) ord[i] = (int32_t)(vt[i] & 0xffffu);
+  }
+}
+
+size_t sort_smem_bytes(int n) { return (size_t)stage_cap(n) * 8; }
 
 // ---------------------------------------------------------------------------
 // Compact result (fast_compact_batch): the changed cells of the balanced
@@ -419,12 +451,6 @@ __global__ void __launch_bounds__(kCompactThreads)
   }
 }
 
-size_t sort_smem_bytes(int n) {
-  int P = 1;
-  while (P < stage_cap(n)) P <<= 1;
-  return (size_t)P * 12;
-}
-
 int check(cudaError_t e) { return e == cudaSuccess ? FAST_OK : FAST_ECUDA; }
 
 int launch_balance(const int64_t* D, int B, int n, int m,
@@ -512,8 +538,8 @@ int launch_decompose(const int64_t* S, int B, int n, int mode, int check_total,
       return FAST_ECUDA;
     sort_granted = ssmem;
   }
-  int threads = (int)(ssmem / 12 / 2);
-  threads = threads < 32 ? 32 : (threads > 1024 ? 1024 : threads);
+  int threads = (stage_cap(n) / 2 + 31) & ~31;
+  threads = threads < 32 ? 32 : (threads > kSortThreads ? kSortThreads : threads);
   sort_kernel<<<B, threads, ssmem, s>>>(n, *out);
   return check(cudaGetLastError());
 }

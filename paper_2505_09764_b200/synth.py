@@ -311,84 +311,159 @@ class HostSchedules:
             n_stages=s, stage_order=self.stage_order[b, :s].numpy())
 
 
-def synthesize_host_batch(D_host: torch.Tensor, n: int, m: int, out: HostSchedules | None = None,
-                          chunk: int = 125, device=None, _cache: dict = {}) -> HostSchedules:
-    """synthesize_fast over a batch held in (pinned) HOST memory, returning
-    the compact host result (HostSchedules).
+class HostSynthPipeline:
+    """synthesize_fast over batches held in (pinned) HOST memory, producing
+    the compact host result (HostSchedules) -- the e2e path.
 
-    The batch is split into chunks, each on its own stream with its own
-    device buffers: chunk i's H2D, synthesis (+ fast_compact_batch) and the
-    D2H of its fixed-size fields are stream-ordered; the chunks are
-    independent, so the copy engines stream inputs and results while every
-    chunk's (latency-bound) decomposition runs concurrently on the SMs.  The
-    variable-length changed-cell values of a chunk are copied once its count
-    has landed on the host.  Returns after the last D2H."""
+    A batch is split into chunks; each chunk has its own stream and device
+    buffers: its H2D, synthesis (+ fast_compact_batch) and the D2H of its
+    fixed-size fields are stream-ordered, and the chunks are independent, so
+    the copy engines stream inputs and results while every chunk's
+    (latency-bound) decomposition runs on the SMs.  The variable-length
+    changed-cell values of a chunk are copied once its count has landed on
+    the host.
+
+    `depth` buffer sets rotate between consecutive batches: ``submit`` only
+    enqueues (returning a ticket) and ``result`` completes a ticket, so a
+    caller streaming batches keeps the next batch's H2D and kernels in flight
+    while the previous batch's chain tail and D2H finish (``run``)."""
+
+    def __init__(self, B: int, n: int, m: int, chunk: int = 125, depth: int = 2, device=None):
+        dev = device or _device()
+        lib = _lib.load()
+        self.B, self.n, self.m, self.dev = B, n, m, dev
+        C = max(1, min(chunk, B))
+        self.starts = list(range(0, B, C))
+        sizes = [min(C, B - b0) for b0 in self.starts]
+        T = n * (n - 1)
+        self.sets = []
+        for _ in range(max(1, depth)):
+            self.sets.append(dict(
+                bufs=[SynthBuffers(nb, n, m, dev, compact=True) for nb in sizes],
+                dins=[torch.empty((nb, n * m, n * m), dtype=torch.int64, device=dev)
+                      for nb in sizes],
+                vals=[torch.empty(nb * max(T, 1) * m * m, dtype=torch.int64, device=dev)
+                      for nb in sizes],
+                base=[torch.empty(nb + 1, dtype=torch.int64, device=dev) for nb in sizes],
+                base_h=[torch.empty(nb + 1, dtype=torch.int64, pin_memory=True) for nb in sizes],
+                ws=[torch.empty(int(lib.fast_compact_workspace_bytes(nb)), dtype=torch.uint8,
+                                device=dev) for nb in sizes],
+                streams=[torch.cuda.Stream(dev) for _ in sizes],
+                events=[torch.cuda.Event() for _ in sizes]))
+        self._next = 0
+
+    def submit(self, D_host: torch.Tensor, out: HostSchedules, trace: list | None = None):
+        """Enqueue one batch (no host synchronisation); returns a ticket."""
+        n, m = self.n, self.m
+        if (D_host.device.type != "cpu" or D_host.dtype != torch.int64 or D_host.dim() != 3
+                or D_host.shape[0] != self.B):
+            raise ValidationError(f"D_host must be a CPU int64 tensor [{self.B}, G, G]")
+        lib = _lib.load()
+        c = self.sets[self._next]
+        self._next = (self._next + 1) % len(self.sets)
+        cur = torch.cuda.current_stream(self.dev)
+        ev = (lambda: torch.cuda.Event(enable_timing=True)) if trace is not None else None
+        if trace is not None:
+            t_start = ev()
+            t_start.record(cur)
+            trace.append(t_start)
+        for i, b0 in enumerate(self.starts):
+            st, nb, bufs = c["streams"][i], c["dins"][i].shape[0], c["bufs"][i]
+            st.wait_stream(cur)
+            with torch.cuda.stream(st):
+                c["dins"][i].copy_(D_host[b0:b0 + nb], non_blocking=True)
+                if trace is not None:
+                    trace.append(("h2d", i, ev()))
+                    trace[-1][2].record(st)
+                sh = ctypes.c_void_p(st.cuda_stream)
+                evs = None
+                if trace is not None:
+                    kev = [ev() for _ in range(4)]
+                    trace.extend([("bal0", i, kev[0]), ("bal1", i, kev[1]), ("dec1", i, kev[2]),
+                                  ("sort1", i, kev[3])])
+                    for e in kev:
+                        e.record(st)  # materialise
+                    evs = (ctypes.c_void_p * 4)(*[e.cuda_event for e in kev])
+                _lib.check_rc(lib.fast_synth_batch_ev(ctypes.c_void_p(c["dins"][i].data_ptr()),
+                                                      nb, n, m, ctypes.byref(bufs.struct), sh,
+                                                      evs), "fast_synth_batch")
+                _lib.check_rc(lib.fast_compact_batch(ctypes.byref(bufs.struct), nb, n, m,
+                                                     ctypes.c_void_p(c["vals"][i].data_ptr()),
+                                                     ctypes.c_void_p(c["base"][i].data_ptr()),
+                                                     ctypes.c_void_p(c["ws"][i].data_ptr()), sh),
+                              "fast_compact_batch")
+                if trace is not None:
+                    trace.append(("synth", i, ev()))
+                    trace[-1][2].record(st)
+                c["base_h"][i].copy_(c["base"][i], non_blocking=True)
+                c["events"][i].record(st)
+                for f in _COMPACT_FIELDS:
+                    getattr(out, f)[b0:b0 + nb].copy_(getattr(bufs, f), non_blocking=True)
+                if trace is not None:
+                    trace.append(("d2h", i, ev()))
+                    trace[-1][2].record(st)
+        return (c, out)
+
+    def result(self, ticket, sync: bool = True) -> HostSchedules:
+        """Complete a ticket: as each chunk's value count lands, enqueue the
+        D2H of its changed-cell values; sync=True waits for the last copy."""
+        c, out = ticket
+        off = 0
+        for i, b0 in enumerate(self.starts):
+            c["events"][i].synchronize()
+            nb = c["dins"][i].shape[0]
+            base = c["base_h"][i]
+            tot = int(base[nb])
+            if off + tot > out.vals.numel():  # grow (first call at this size)
+                for st in c["streams"]:
+                    st.synchronize()
+                grown = torch.empty(max(2 * out.vals.numel(), off + tot), dtype=torch.int64,
+                                    pin_memory=True)
+                grown[:off].copy_(out.vals[:off])
+                out.vals = grown
+            with torch.cuda.stream(c["streams"][i]):
+                if tot:
+                    out.vals[off:off + tot].copy_(c["vals"][i][:tot], non_blocking=True)
+            out.val_base[b0:b0 + nb] = base[:nb] + off
+            off += tot
+        out.val_base[self.B] = off
+        out.n_vals = off
+        if sync:
+            for st in c["streams"]:
+                st.synchronize()
+        return out
+
+    def run(self, batches, outs) -> list[HostSchedules]:
+        """Stream batches through the pipeline: batch t+1 is enqueued before
+        batch t is completed.  outs[t] receives batch t (reuse two objects
+        alternately for a steady stream)."""
+        pending, done = None, []
+        for D_host, out in zip(batches, outs):
+            t = self.submit(D_host, out)
+            if pending is not None:
+                done.append(self.result(pending))
+            pending = t
+        if pending is not None:
+            done.append(self.result(pending))
+        return done
+
+
+def synthesize_host_batch(D_host: torch.Tensor, n: int, m: int, out: HostSchedules | None = None,
+                          chunk: int = 125, device=None, _cache: dict = {},
+                          trace: list | None = None) -> HostSchedules:
+    """synthesize_fast over one batch in (pinned) HOST memory, synchronously
+    (HostSynthPipeline with one buffer set, cached across calls)."""
     dev = device or _device()
     if D_host.device.type != "cpu" or D_host.dtype != torch.int64 or D_host.dim() != 3:
         raise ValidationError("D_host must be a CPU int64 tensor [B, G, G]")
     B = D_host.shape[0]
     out = out or HostSchedules(B, n, m)
-    lib = _lib.load()
-    C = max(1, min(chunk, B))
-    starts = list(range(0, B, C))
-    T = n * (n - 1)
-    key = (str(dev), B, n, m, C)
+    key = (str(dev), B, n, m, max(1, min(chunk, B)))
     if key not in _cache:  # device buffers and streams are reused across calls
         _cache.clear()
-        sizes = [min(C, B - b0) for b0 in starts]
-        _cache[key] = dict(
-            bufs=[SynthBuffers(nb, n, m, dev, compact=True) for nb in sizes],
-            dins=[torch.empty((nb, n * m, n * m), dtype=torch.int64, device=dev) for nb in sizes],
-            vals=[torch.empty(nb * max(T, 1) * m * m, dtype=torch.int64, device=dev)
-                  for nb in sizes],
-            base=[torch.empty(nb + 1, dtype=torch.int64, device=dev) for nb in sizes],
-            base_h=[torch.empty(nb + 1, dtype=torch.int64, pin_memory=True) for nb in sizes],
-            ws=[torch.empty(int(lib.fast_compact_workspace_bytes(nb)), dtype=torch.uint8,
-                            device=dev) for nb in sizes],
-            streams=[torch.cuda.Stream(dev) for _ in starts],
-            events=[torch.cuda.Event() for _ in starts])
-    c = _cache[key]
-    cur = torch.cuda.current_stream(dev)
-    for i, b0 in enumerate(starts):
-        st, nb, bufs = c["streams"][i], c["dins"][i].shape[0], c["bufs"][i]
-        st.wait_stream(cur)
-        with torch.cuda.stream(st):
-            c["dins"][i].copy_(D_host[b0:b0 + nb], non_blocking=True)
-            sh = ctypes.c_void_p(st.cuda_stream)
-            _lib.check_rc(lib.fast_synth_batch(ctypes.c_void_p(c["dins"][i].data_ptr()), nb, n, m,
-                                               ctypes.byref(bufs.struct), sh), "fast_synth_batch")
-            _lib.check_rc(lib.fast_compact_batch(ctypes.byref(bufs.struct), nb, n, m,
-                                                 ctypes.c_void_p(c["vals"][i].data_ptr()),
-                                                 ctypes.c_void_p(c["base"][i].data_ptr()),
-                                                 ctypes.c_void_p(c["ws"][i].data_ptr()), sh),
-                          "fast_compact_batch")
-            c["base_h"][i].copy_(c["base"][i], non_blocking=True)
-            c["events"][i].record(st)
-            for f in _COMPACT_FIELDS:
-                getattr(out, f)[b0:b0 + nb].copy_(getattr(bufs, f), non_blocking=True)
-    off = 0
-    for i, b0 in enumerate(starts):
-        c["events"][i].synchronize()
-        nb = c["dins"][i].shape[0]
-        base = c["base_h"][i]
-        tot = int(base[nb])
-        if off + tot > out.vals.numel():  # grow (first call at this size)
-            for st in c["streams"]:
-                st.synchronize()
-            grown = torch.empty(max(2 * out.vals.numel(), off + tot), dtype=torch.int64,
-                                pin_memory=True)
-            grown[:off].copy_(out.vals[:off])
-            out.vals = grown
-        with torch.cuda.stream(c["streams"][i]):
-            if tot:
-                out.vals[off:off + tot].copy_(c["vals"][i][:tot], non_blocking=True)
-        out.val_base[b0:b0 + nb] = base[:nb] + off
-        off += tot
-    out.val_base[B] = off
-    out.n_vals = off
-    for st in c["streams"]:
-        st.synchronize()
-    return out
+        _cache[key] = HostSynthPipeline(B, n, m, chunk, depth=1, device=dev)
+    pipe = _cache[key]
+    return pipe.result(pipe.submit(D_host, out, trace))
 
 
 # ---------------------------------------------------------------------------
