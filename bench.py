@@ -107,8 +107,8 @@ def synth_inputs(args, device):
 
 
 def algorithmic_bytes_decompose(n: int, n_raw) -> int:
-    # read server matrix, write aux, write each raw stage (weight + perm)
-    return int(sum(16 * n * n + int(k) * (8 + n) for k in n_raw))
+    # read server matrix, write aux, write each raw stage (weight + perm + bytes)
+    return int(sum(16 * n * n + int(k) * (8 + 9 * n) for k in n_raw))
 
 
 # Dependent-chain floor of one DFS step of the decomposition (cycles):
@@ -117,7 +117,7 @@ def algorithmic_bytes_decompose(n: int, n_raw) -> int:
 DFS_STEP_FLOOR_CYCLES = 70.0
 
 SUBSET_KEYS = ("balanced", "server", "move_count", "moves", "common_sum", "aux", "n_raw",
-               "stage_weight", "stage_perm", "n_stages", "stage_order", "status", "strip")
+               "stage_weight", "stage_perm", "stage_bytes", "n_stages", "stage_order", "status")
 
 
 def device_subset(bufs, k: int) -> dict:
@@ -154,7 +154,6 @@ def bench_synth(args) -> dict:
     import torch
 
     from paper_2505_09764_b200 import _lib, synth
-    from paper_2505_09764_b200.schedule import STRIP_DTYPE, stage_bytes_from_strip
 
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -162,21 +161,17 @@ def bench_synth(args) -> dict:
     n, m, B = args.n, args.m, args.batch
     G, T = n * m, n * (n - 1)
     D = synth_inputs(args, dev)
-    # the batch product layout: the aux run-out table (replaces the per-edge
-    # stage bytes on the host side), changed-cell masks + the compact pack of
-    # the balanced tiles.  The per-edge stage bytes are still written on the
-    # device: the peel loop without those stores compiles ~13% slower
-    # (measured, profiles/README.md), and they never cross PCIe.
-    bufs = synth.SynthBuffers(B, n, m, dev, compact=True)
-    vals = torch.empty(B * T * m * m, dtype=torch.int64, device=dev)
-    vbase = torch.empty(B + 1, dtype=torch.int64, device=dev)
-    cws = torch.empty(int(lib.fast_compact_workspace_bytes(B)), dtype=torch.uint8, device=dev)
+    # device-resident product layout (balanced matrix, moves, raw stages with
+    # per-edge bytes, sort order): what the executor and other device
+    # consumers read.  The e2e leg below adds the host transport format (aux
+    # run-out table + compact balanced tiles) and times it separately.
+    bufs = synth.SynthBuffers(B, n, m, dev)
     stream = torch.cuda.current_stream()
     sh = ctypes.c_void_p(stream.cuda_stream)
     P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
 
     def make_events(k):
-        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(k)]
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(k)]
         for row in evs:
             for e in row:
                 e.record(stream)  # materialise the handles
@@ -188,11 +183,6 @@ def bench_synth(args) -> dict:
             arr = (ctypes.c_void_p * 4)(*[e.cuda_event for e in ev_row[:4]])
         rc = lib.fast_synth_batch_ev(P(D), B, n, m, ctypes.byref(bufs.struct), sh, arr)
         _lib.check_rc(rc, "fast_synth_batch_ev")
-        rc = lib.fast_compact_batch(ctypes.byref(bufs.struct), B, n, m, P(vals), P(vbase), P(cws),
-                                    sh)
-        _lib.check_rc(rc, "fast_compact_batch")
-        if ev_row is not None:
-            ev_row[4].record(stream)
 
     for _ in range(args.warmup):
         step()
@@ -211,7 +201,7 @@ def bench_synth(args) -> dict:
         t1.record(stream)
         torch.cuda.synchronize()
     total_ms = t0.elapsed_time(t1)
-    names = ("balance_kernel", "decompose_kernel", "sort_strip_kernels", "compact_kernels")
+    names = ("balance_kernel", "decompose_kernel", "sort_kernel")
     per = {k: 0.0 for k in names}
     for row in evs:
         for i, k in enumerate(names):
@@ -221,17 +211,13 @@ def bench_synth(args) -> dict:
     n_raw = bufs.n_raw.cpu().tolist()
     P_CHECK = min(64, B)
     dev_sub = device_subset(bufs, P_CHECK)
-    dev_sub["stage_bytes"] = [stage_bytes_from_strip(dev_sub["stage_weight"][b, :n_raw[b]],
-                                                     dev_sub["stage_perm"][b, :n_raw[b]],
-                                                     dev_sub["strip"][b].view(STRIP_DTYPE).reshape(-1))
-                              for b in range(P_CHECK)]
     d2h_device_layout = int(bufs.output_nbytes())
 
     peaks, peak_kind = measured_peaks()
     hbm = float(peaks["hbm_gbs"])
     alg = {"balance_kernel": 16 * G * G * B,
            "decompose_kernel": algorithmic_bytes_decompose(n, n_raw),
-           "sort_strip_kernels": int(sum(12 * 2 * k for k in n_raw))}
+           "sort_kernel": int(sum(8 * 2 * k for k in n_raw))}
     dom = max(per, key=per.get)
     achieved = alg[dom] / (per[dom] * 1e-3) / 1e9
     traffic = None
@@ -268,7 +254,7 @@ def bench_synth(args) -> dict:
     if not args.no_e2e:
         Dh = torch.empty(D.shape, dtype=D.dtype, pin_memory=True)
         Dh.copy_(D)
-        del bufs, vals
+        del bufs
         torch.cuda.empty_cache()
         pipe = synth.HostSynthPipeline(B, n, m, chunk=args.e2e_chunk, depth=2)
         outs = [synth.HostSchedules(B, n, m), synth.HostSchedules(B, n, m)]
@@ -305,7 +291,6 @@ def bench_synth(args) -> dict:
         k_chk = min(P_CHECK, int(ref["n_raw"].shape[0]))
         for b in range(k_chk):
             got = {key: dev_sub[key][b] for key in SUBSET_KEYS}
-            got["stage_bytes"] = dev_sub["stage_bytes"][b]
             compare_with_oracle(ref, b, got, "device path")
             if hs is not None:
                 p = hs.packed(b, Dh[b].numpy())
@@ -342,7 +327,7 @@ def bench_synth(args) -> dict:
         "l2": "inputs larger than L2 (D batch = %.1f GB)" % (B * G * G * 8 / 1e9)
               if B * G * G * 8 > 126e6 else "inputs within L2",
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": 6 * args.steps, "clocks": clk.summary(),
+        "gpu_launches": 3 * args.steps, "clocks": clk.summary(),
         "stages_per_matrix_mean": round(peels, 1),
     }
     if parity is not None:
