@@ -32,6 +32,9 @@ import numpy as np
 # the e2e path streams batches over 2 x 8 chunk streams: give each its own
 # hardware queue (must be set before the CUDA context exists)
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# rank 0 prints exactly one JSON line: keep NCCL's version banner off stdout
+if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+    os.environ["NCCL_DEBUG"] = "WARN"
 
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
@@ -497,6 +500,8 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--nccl-only", action="store_true")
+    ap.add_argument("--experts", type=int, default=8)
     ap.add_argument("--e2e-chunk", type=int, default=125)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup

@@ -36,6 +36,92 @@ def demand(args, world: int) -> np.ndarray:
     return workloads.zipf_sizes(args.seed, world, args.a2a_skew, args.a2a_total)
 
 
+class NvlinkCounters:
+    """NVML NVLink data throughput counters (KiB, cumulative, summed over the
+    GPU's links) for the GPU behind a CUDA device index -- ncu cannot replay
+    the exec kernel (its ranks wait on each other), NVML counts the wire
+    traffic of the real multi-rank run."""
+
+    FIELD_TX, FIELD_RX = 138, 139  # NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX
+
+    def __init__(self, device_index: int):
+        self.h = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            p = torch.cuda.get_device_properties(device_index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            self.links = [l for l in range(18)
+                          if self._state(l)]
+        except Exception:  # pragma: no cover - NVML absent
+            self.h = None
+
+    def _state(self, link: int) -> bool:
+        try:
+            return self.nv.nvmlDeviceGetNvLinkState(self.h, link) == 1
+        except Exception:
+            return False
+
+    def read(self):
+        """(tx_bytes, rx_bytes) or None."""
+        if self.h is None or not self.links:
+            return None
+        try:
+            ids = [(self.FIELD_TX, l) for l in self.links] + [(self.FIELD_RX, l) for l in self.links]
+            vals = self.nv.nvmlDeviceGetFieldValues(self.h, ids)
+            tot = [0, 0]
+            for i, v in enumerate(vals):
+                if v.nvmlReturn != 0:
+                    return None
+                tot[0 if i < len(self.links) else 1] += int(v.value.ullVal)
+            return tot[0] * 1024, tot[1] * 1024
+        except Exception:
+            return None
+
+
+def peer_copy_peaks(comm, rank: int, nbytes: int) -> dict | None:
+    """In-run NVLink push peaks, rank 0 -> rank 1's receive region: the
+    executor's SM copy loop (fast_debug_copy, 128 CTAs) and the copy engine
+    (cudaMemcpyAsync); GB/s per direction, best of 5 (other ranks idle)."""
+    import ctypes
+
+    from paper_2505_09764_b200 import _lib
+
+    lib = _lib.load()
+    res = None
+    dist.barrier()
+    if rank == 0:
+        dst = lib.fast_comm_peer_ptr(comm._ptr, 1)
+        recv_off = lib.fast_comm_recv_ptr(comm._ptr) - lib.fast_comm_peer_ptr(comm._ptr, 0)
+        src = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        s = torch.cuda.current_stream()
+        out = {}
+        for name in ("sm_copy", "copy_engine"):
+            best = 1e9
+            for _ in range(6):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                if name == "sm_copy":
+                    lib.fast_debug_copy(ctypes.c_void_p(dst + recv_off),
+                                        ctypes.c_void_p(src.data_ptr()), nbytes, 128, 1 << 20, 1,
+                                        ctypes.c_void_p(s.cuda_stream))
+                else:
+                    lib.fast_debug_memcpy(ctypes.c_void_p(dst + recv_off),
+                                          ctypes.c_void_p(src.data_ptr()), nbytes,
+                                          ctypes.c_void_p(s.cuda_stream))
+                b.record(s)
+                b.synchronize()
+                best = min(best, a.elapsed_time(b))
+            out[name] = round(nbytes / (best * 1e-3) / 1e9, 1)
+        res = {"bytes": nbytes, "GBps": out, "what": "push rank0 -> rank1, best of 5"}
+    torch.cuda.synchronize()
+    dist.barrier()
+    return res
+
+
 def fast_wire_bytes(ops: np.ndarray, G: int) -> tuple[int, int]:
     eg = np.zeros(G, np.int64)
     ing = np.zeros(G, np.int64)
@@ -62,6 +148,8 @@ def run(args, workload: str) -> dict | None:
     n, m = topology_for(world, args.topo)
     D = demand(args, world)
     G = world
+    if getattr(args, "nccl_only", False):
+        return nccl_only(args, D, rank, world)
     total = int(D.sum())
     cap = int(max(D.sum(0).max(), D.sum(1).max())) + 4096
     comm = FastComm(Topology(n, m), recv_bytes=cap, staging_bytes=2 * cap + (4 << 20),
@@ -99,17 +187,32 @@ def run(args, workload: str) -> dict | None:
         torch.cuda.synchronize()
     comm.check()
     step_ms = t0.elapsed_time(t1) / args.steps
-    # exec kernel alone (same traffic, step-by-step path with events around it)
+    # exec kernel alone (same traffic, step-by-step path with events around it),
+    # with the NVML NVLink data counters read around the loop
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
+    nvl = NvlinkCounters(local)
+    torch.cuda.synchronize()
+    dist.barrier()
+    c0 = nvl.read()
     for k in range(args.steps):
         comm.alltoallv(send, row, exec_events=ev[k])
     torch.cuda.synchronize()
+    c1 = nvl.read()
+    dist.barrier()
     comm.check()
     exec_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    my_exec_ms = exec_ms
     mx = torch.tensor([step_ms, exec_ms], device="cuda")
     dist.all_reduce(mx, op=dist.ReduceOp.MAX)
     step_ms, exec_ms = (float(x) for x in mx.tolist())
+    nvl_rank = None
+    if c0 is not None and c1 is not None:
+        tx, rx = (c1[0] - c0[0]) / args.steps, (c1[1] - c0[1]) / args.steps
+        nvl_rank = [tx, rx, my_exec_ms]
+    nvl_all = [None] * world
+    dist.all_gather_object(nvl_all, nvl_rank)
+    peaks_run = peer_copy_peaks(comm, rank, min(comm.recv_bytes - 4096, 128 << 20))
 
     # NCCL all_to_all_single on the identical traffic (practical B200 bar)
     ins, outs = D[rank].tolist(), D[:, rank].tolist()
@@ -196,11 +299,58 @@ def run(args, workload: str) -> dict | None:
                     "path": "FastComm.alltoallv with pinned host send/recv (rank-0 bytes)"},
             "gpu_launches": 6 * args.steps, "clocks": clk.summary(),
             "parity": "recv == NCCL all_to_all_single bytes on every rank",
+            "peer_copy_peak_in_run": peaks_run,
         }
+        if all(x is not None for x in nvl_all):
+            per = [{"rank": r, "tx_GB": round(x[0] / 1e9, 4), "rx_GB": round(x[1] / 1e9, 4),
+                    "tx_GBps": round(x[0] / (x[2] * 1e-3) / 1e9, 1),
+                    "rx_GBps": round(x[1] / (x[2] * 1e-3) / 1e9, 1)} for r, x in enumerate(nvl_all)]
+            res["nvlink_counters"] = {
+                "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX around the exec-only loop, per "
+                          "exec call; GB/s over the rank's own exec-kernel event time",
+                "per_rank": per,
+                "max_rx_GBps_of_900": round(max(p["rx_GBps"] for p in per) / NVLINK_NOMINAL, 4),
+                "wire_bytes_vs_plan": round(max(x[1] for x in nvl_all) / max(fast_in, 1), 4)}
+        if peaks_run:
+            pk = peaks_run["GBps"]["sm_copy"]
+            res["roofline"]["frac_of_in_run_sm_peak"] = round(
+                direct_bn / (pk * 1e9) / (exec_ms * 1e-3), 4)
     comm.close()
     dist.barrier()
     dist.destroy_process_group()
     return res
+
+
+NCCL_KNOBS = ("NCCL_NCHANNELS_PER_PEER", "NCCL_MIN_P2P_NCHANNELS", "NCCL_MAX_P2P_NCHANNELS",
+              "NCCL_MIN_NCHANNELS", "NCCL_MAX_NCHANNELS", "NCCL_P2P_NVL_CHUNKSIZE",
+              "NCCL_BUFFSIZE", "NCCL_NVLS_ENABLE", "NCCL_P2P_LEVEL")
+
+
+def nccl_only(args, D: np.ndarray, rank: int, world: int) -> dict | None:
+    """NCCL all_to_all_single alone on the config-2 traffic, with the NCCL
+    environment of this process recorded (tools/nccl_sweep.sh varies it)."""
+    ins, outs = D[rank].tolist(), D[:, rank].tolist()
+    sv = torch.randint(0, 256, (int(D[rank].sum()),), dtype=torch.uint8, device="cuda")
+    out = torch.empty(int(D[:, rank].sum()), dtype=torch.uint8, device="cuda")
+    for _ in range(max(3, args.warmup)):
+        dist.all_to_all_single(out, sv, outs, ins)
+    torch.cuda.synchronize()
+    dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.steps):
+        dist.all_to_all_single(out, sv, outs, ins)
+    b.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([a.elapsed_time(b) / args.steps], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    dist.destroy_process_group()
+    if rank:
+        return None
+    return {"what": "nccl_all_to_all_single", "n_gpus": world, "ms": round(ms, 4),
+            "GBps": round(int(D.sum()) / (ms * 1e-3) / 1e9, 2),
+            "env": {k: os.environ[k] for k in NCCL_KNOBS if k in os.environ}}
 
 
 def reference_alltoallv(args, world: int) -> dict:
@@ -263,8 +413,8 @@ def reference_alltoallv(args, world: int) -> dict:
 
 
 def run_moe(args) -> dict | None:
-    """BASELINE config 3: Mixtral-style dispatch, E = N experts (one per GPU),
-    top-2, 16k tokens x 4096 bf16 per GPU.  One step = gating -> histogram ->
+    """BASELINE config 3: Mixtral-style dispatch, E = 8 experts (--experts;
+    E / N per GPU), top-2, 16k tokens x 4096 bf16 per GPU.  One step = gating -> histogram ->
     demand all-gather -> FAST synthesis -> pack -> P2P alltoallv -> unpack."""
     from paper_2505_09764_b200 import Topology
     from paper_2505_09764_b200.executor import FastComm
@@ -278,10 +428,11 @@ def run_moe(args) -> dict | None:
     n, m = topology_for(world, args.topo)
     T, hidden = args.tokens, args.hidden
     RB = hidden * 2
-    cap = T * 2 * RB * 2  # generous: a hot expert can receive 2x its share
+    cap = T * 2 * RB * 3  # generous: the hot experts' rank can receive 3x its share
     comm = FastComm(Topology(n, m), recv_bytes=cap, staging_bytes=cap, blocks=args.blocks,
                     chunk_bytes=args.chunk)
-    disp = MoEDispatch(comm, T, RB)
+    E = args.experts if args.experts % world == 0 else world
+    disp = MoEDispatch(comm, T, RB, num_experts=E)
     gen = torch.Generator(device="cuda").manual_seed(7 + rank)
     tokens = torch.randn(T, hidden, dtype=torch.bfloat16, device="cuda", generator=gen)
     stream = torch.cuda.current_stream()
@@ -317,7 +468,7 @@ def run_moe(args) -> dict | None:
     ms = float(ms.item())
     # fused pack -> send (row-mapped executor source): same expert input, no
     # packed send buffer written or read
-    fdisp = MoEDispatch(comm, T, RB, fused_pack=True)
+    fdisp = MoEDispatch(comm, T, RB, fused_pack=True, num_experts=E)
     frecv = fdisp.dispatch(tokens, seed=args.seed)
     torch.cuda.synchronize()
     comm.check()
@@ -392,7 +543,8 @@ def run_moe(args) -> dict | None:
                "vs_baseline": None, "dtype": "bf16 payload (bytes moved as u8)",
                "data": "synthetic tokens, deterministic integer top-2 gating",
                "config": {"workload": "config3_moe_dispatch", "virtual_servers": f"{n}x{m}",
-                          "experts": world, "top_k": 2, "tokens_per_gpu": T,
+                          "experts": E, "experts_per_gpu": E // world, "top_k": 2,
+                          "tokens_per_gpu": T,
                           "hidden": hidden, "cross_gpu_bytes": cross,
                           "bottleneck_gpu_bytes": bn},
                "t_roof_us": round(bn / (PEER_GBS * 1e9) * 1e6, 1),

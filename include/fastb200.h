@@ -348,6 +348,10 @@ void *fast_comm_peer_ptr(const fast_comm *c, int rank);
 int fast_debug_copy(void *dst, const void *src, int64_t bytes, int blocks,
                     int64_t chunk, int nc, void *stream);
 
+/* Diagnostics: a copy-engine copy (cudaMemcpyAsync) of the same bytes, for
+ * the in-run SM-store vs copy-engine NVLink peak measurement. */
+int fast_debug_memcpy(void *dst, const void *src, int64_t bytes, void *stream);
+
 /* Device status word of the last exec on this comm: 0 ok, 2 = the counts
  * overran the send capacity (fast_comm_set_send_capacity), 3 = a wait timed
  * out (peers missing or protocol error).  A non-zero status is sticky and

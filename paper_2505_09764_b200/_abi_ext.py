@@ -64,6 +64,7 @@ SIGNATURES: list[tuple[str, object, list]] = [
     ("fast_comm_set_send_rows", I, [V, V, V, I64, I64]),
     ("fast_comm_set_send_capacity", I, [V, I64]),
     ("fast_debug_copy", I, [V, V, I64, I, I64, I, V]),
+    ("fast_debug_memcpy", I, [V, V, I64, V]),
     ("fast_comm_create_group", I, [I, I64, I64, ctypes.POINTER(V)]),
     ("fast_exec_group", I, [ctypes.POINTER(V), I, P_PLAN, ctypes.POINTER(V), I64, I, I64, V, V]),
     # stage-level building blocks (stages.cu)

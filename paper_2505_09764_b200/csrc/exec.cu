@@ -1091,6 +1091,14 @@ int fast_debug_copy(void* dst, const void* src, int64_t bytes, int blocks, int64
   return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
 }
 
+int fast_debug_memcpy(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (!dst || !src || bytes < 0) return FAST_EVALIDATION;
+  return cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice,
+                         (cudaStream_t)stream) == cudaSuccess
+             ? FAST_OK
+             : FAST_ECUDA;
+}
+
 // Single-launch fused path (n <= 6): gather, synthesis and plan run in CTA 0
 // of the exec kernel itself.
 static int launch_fused(fast_comm* c, const void* send, const int64_t* counts, int n, int m,
