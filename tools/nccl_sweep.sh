@@ -8,11 +8,9 @@ run() {
     --nccl-only 2>/dev/null | tail -1
 }
 run X=1
-run NCCL_NCHANNELS_PER_PEER=4
-run NCCL_NCHANNELS_PER_PEER=8
-run NCCL_NCHANNELS_PER_PEER=16
-run NCCL_MIN_P2P_NCHANNELS=32 NCCL_MAX_P2P_NCHANNELS=64
-run NCCL_MIN_P2P_NCHANNELS=32 NCCL_MAX_P2P_NCHANNELS=64 NCCL_NCHANNELS_PER_PEER=16
-run NCCL_MIN_P2P_NCHANNELS=64 NCCL_MAX_P2P_NCHANNELS=64 NCCL_NCHANNELS_PER_PEER=32
-run NCCL_P2P_NVL_CHUNKSIZE=2097152 NCCL_NCHANNELS_PER_PEER=16 NCCL_MIN_P2P_NCHANNELS=32
-run NCCL_BUFFSIZE=16777216 NCCL_NCHANNELS_PER_PEER=16 NCCL_MIN_P2P_NCHANNELS=32
+run NCCL_NCHANNELS_PER_PEER=32
+run NCCL_NCHANNELS_PER_PEER=32 NCCL_MIN_P2P_NCHANNELS=32 NCCL_MAX_P2P_NCHANNELS=32
+run NCCL_NCHANNELS_PER_PEER=32 NCCL_MIN_P2P_NCHANNELS=64 NCCL_MAX_P2P_NCHANNELS=64
+run NCCL_NCHANNELS_PER_PEER=64 NCCL_MIN_P2P_NCHANNELS=64 NCCL_MAX_P2P_NCHANNELS=64
+run NCCL_NCHANNELS_PER_PEER=32 NCCL_MIN_P2P_NCHANNELS=64 NCCL_MAX_P2P_NCHANNELS=64 NCCL_P2P_NVL_CHUNKSIZE=1048576
+run NCCL_NCHANNELS_PER_PEER=16 NCCL_MIN_P2P_NCHANNELS=64 NCCL_MAX_P2P_NCHANNELS=64
