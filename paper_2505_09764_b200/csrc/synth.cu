@@ -175,6 +175,144 @@ __global__ void __launch_bounds__(kBalThreads)
 }
 
 
+// ---------------------------------------------------------------------------
+// balance_tma_kernel (opt-in, -DFAST_BAL_TMA; slower, see launch_balance):
+// the same per-tile work as balance_kernel, as a persistent pipeline fed by
+// the TMA engine.  Each thread owns one m x m tile
+// slot per buffer (tile-major, padded) and runs its own two-deep pipeline:
+// the m tile rows of its NEXT tile are fetched with 1-D bulk copies
+// (cp.async.bulk ... mbarrier::complete_tx) into the other buffer while it
+// balances the current one, and the balanced rows go back with bulk stores
+// (cp.async.bulk.global.shared::cta).  No CTA-wide barrier: every thread
+// waits only on its own mbarrier, so the HBM stream never stalls behind the
+// slowest greedy of a strip.  grid = resident CTAs, block = kTmaTiles.
+constexpr int kTmaTiles = 64;  // tiles (threads) per CTA
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n\t}" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+      "r"(phase) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* smem, const void* gmem, unsigned bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem), "r"(bytes),
+      "r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gmem, const void* smem, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem),
+               "r"((uint32_t)__cvta_generic_to_shared(smem)), "r"(bytes) : "memory");
+}
+
+template <int M>
+__global__ void __launch_bounds__(kTmaTiles)
+    balance_tma_kernel(const int64_t* __restrict__ D, const int n, const int B,
+                       fast_sched_bufs out) {
+  constexpr int TS = M * M + 2;  // int64 per tile slot: 16-byte aligned, banks staggered
+  extern __shared__ __align__(128) int64_t tsm[];
+  __shared__ __align__(8) uint64_t bars[2][kTmaTiles];
+  const int jj = threadIdx.x;
+  const int64_t G = (int64_t)n * M;
+  const int nj = (n + kTmaTiles - 1) / kTmaTiles;  // strips per server row
+  const int64_t items = (int64_t)B * n * nj;
+  mbar_init(&bars[0][jj], 1);
+  mbar_init(&bars[1][jj], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const int slots = M > 1 ? M - 1 : 1;
+  const int T = n * (n - 1);
+
+  // item -> (b, i, j) of this thread's tile; valid = j < n
+  auto tile_of = [&](int64_t it, int& b, int& i, int& j) {
+    b = (int)(it / ((int64_t)n * nj));
+    const int64_t r = it - (int64_t)b * n * nj;
+    i = (int)(r / nj);
+    j = (int)(r - (int64_t)i * nj) * kTmaTiles + jj;
+  };
+  auto fetch = [&](int64_t it, int k) {
+    int b, i, j;
+    tile_of(it, b, i, j);
+    if (j >= n) return;
+    const int64_t* src = D + (int64_t)b * G * G + (int64_t)i * M * G + (int64_t)j * M;
+    mbar_expect_tx(&bars[k][jj], M * M * 8);
+    int64_t* sl = tsm + (int64_t)(k * kTmaTiles + jj) * TS;
+#pragma unroll
+    for (int p = 0; p < M; ++p) bulk_load(sl + p * M, src + p * G, M * 8, &bars[k][jj]);
+  };
+
+  int64_t it = blockIdx.x;
+  if (it < items) fetch(it, 0);
+  unsigned phase[2] = {0u, 0u};
+  for (int k = 0; it < items; it += gridDim.x, k ^= 1) {
+    const int64_t nxt = it + gridDim.x;
+    if (nxt < items) {
+      // the next tile goes into the other slot: its previous bulk store must
+      // have finished reading it
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      fetch(nxt, k ^ 1);
+    }
+    int b, i, j;
+    tile_of(it, b, i, j);
+    if (j >= n) continue;
+    mbar_wait(&bars[k][jj], phase[k]);
+    phase[k] ^= 1u;
+    int64_t* t = tsm + (int64_t)(k * kTmaTiles + jj) * TS;
+    int32_t* st = out.status + b;
+    int64_t rs[M];
+    bool bad = false;
+    int64_t s = 0, tp = 0;
+#pragma unroll
+    for (int p = 0; p < M; ++p) {
+      int64_t r = 0;
+#pragma unroll
+      for (int q = 0; q < M; ++q) {
+        const int64_t v = t[p * M + q];
+        r += v;
+        if (v < 0) { bad = true; continue; }
+        if (i == j && p == q && v != 0) bad = true;
+        s = sat_add(s, v);
+      }
+      rs[p] = r;
+      tp += r;
+    }
+    out.server[(int64_t)b * n * n + i * n + j] = s;
+    if (bad) {
+      raise_status(st, FAST_EVALIDATION);
+    } else if (i != j) {
+      const int tidx = i * (n - 1) + (j < i ? j : j - 1);
+      fast_move* mv = out.moves + ((int64_t)b * T + tidx) * slots;
+      uint64_t mk = 0;
+      int nm = balance_tile<M>(t, M, mv, slots, rs, &mk);
+      if (out.tile_mask) out.tile_mask[(int64_t)b * T + tidx] = mk;
+      if (nm < 0) {
+        raise_status(st, FAST_EINVARIANT);
+        nm = 0;
+      } else if (tp != s) {
+        raise_status(st, FAST_EINVARIANT);
+      }
+      out.move_count[(int64_t)b * T + tidx] = nm;
+    }
+    // generic-proxy writes of the tile -> visible to the bulk (async) proxy
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    int64_t* dst = out.balanced + (int64_t)b * G * G + (int64_t)i * M * G + (int64_t)j * M;
+#pragma unroll
+    for (int p = 0; p < M; ++p) bulk_store(dst + p * G, t + p * M, M * 8);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // One warp per matrix (decompose_one, synth_dev.cuh).
 template <int NW, bool WB>
 __global__ void __launch_bounds__(kDecWarps * 32)
@@ -453,8 +591,39 @@ __global__ void __launch_bounds__(kCompactThreads)
 
 int check(cudaError_t e) { return e == cudaSuccess ? FAST_OK : FAST_ECUDA; }
 
+template <int M>
+int launch_balance_tma(const int64_t* D, int B, int n, const fast_sched_bufs* out,
+                       cudaStream_t s) {
+  const size_t smem = (size_t)2 * kTmaTiles * (M * M + 2) * 8;
+  static int grid = 0;
+  if (!grid) {
+    if (cudaFuncSetAttribute(balance_tma_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return FAST_ECUDA;
+    int dev = 0, sms = 0, per_sm = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, balance_tma_kernel<M>, kTmaTiles,
+                                                      smem) != cudaSuccess)
+      return FAST_ECUDA;
+    grid = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const int64_t items = (int64_t)B * n * ((n + kTmaTiles - 1) / kTmaTiles);
+  const int g = items < grid ? (int)items : grid;
+  balance_tma_kernel<M><<<g, kTmaTiles, smem, s>>>(D, n, B, *out);
+  return check(cudaGetLastError());
+}
+
 int launch_balance(const int64_t* D, int B, int n, int m,
                    const fast_sched_bufs* out, cudaStream_t s) {
+#ifdef FAST_BAL_TMA
+  // opt-in: the TMA-fed per-thread pipeline.  Measured 2.3x SLOWER than the
+  // staged kernel below (13.0 vs 5.6 ms at n=128 x 8, B=1000;
+  // profiles/r2_balance_tma_ab.log): one 64-byte bulk copy per tile row is
+  // 262M TMA operations per batch, and the TMA issue rate, not HBM, bounds it.
+  if (m == 8 && n >= kTmaTiles && (int64_t)B * n >= 2048)
+    return launch_balance_tma<8>(D, B, n, out, s);
+#endif
   const size_t tile_bytes = (size_t)(m * m + 1) * 8;
   // ~32 KiB strips: several CTAs per SM overlap the per-tile sequential
   // balancing of one CTA with the HBM traffic of the others.
