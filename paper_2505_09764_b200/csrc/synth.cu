@@ -175,6 +175,7 @@ __global__ void __launch_bounds__(kBalThreads)
 }
 
 
+#ifdef FAST_BAL_TMA
 // ---------------------------------------------------------------------------
 // balance_tma_kernel (opt-in, -DFAST_BAL_TMA; slower, see launch_balance):
 // the same per-tile work as balance_kernel, as a persistent pipeline fed by
@@ -312,6 +313,8 @@ __global__ void __launch_bounds__(kTmaTiles)
   }
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
+
+#endif  // FAST_BAL_TMA
 
 // One warp per matrix (decompose_one, synth_dev.cuh).
 template <int NW, bool WB>
@@ -591,6 +594,7 @@ __global__ void __launch_bounds__(kCompactThreads)
 
 int check(cudaError_t e) { return e == cudaSuccess ? FAST_OK : FAST_ECUDA; }
 
+#ifdef FAST_BAL_TMA
 template <int M>
 int launch_balance_tma(const int64_t* D, int B, int n, const fast_sched_bufs* out,
                        cudaStream_t s) {
@@ -613,6 +617,8 @@ int launch_balance_tma(const int64_t* D, int B, int n, const fast_sched_bufs* ou
   balance_tma_kernel<M><<<g, kTmaTiles, smem, s>>>(D, n, B, *out);
   return check(cudaGetLastError());
 }
+
+#endif  // FAST_BAL_TMA
 
 int launch_balance(const int64_t* D, int B, int n, int m,
                    const fast_sched_bufs* out, cudaStream_t s) {
