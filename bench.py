@@ -168,9 +168,16 @@ def bench_synth(args) -> dict:
     # per-edge bytes, sort order): what the executor and other device
     # consumers read.  The e2e leg below adds the host transport format (aux
     # run-out table + compact balanced tiles) and times it separately.
-    bufs = synth.SynthBuffers(B, n, m, dev)
+    # `inflight` batches are processed concurrently (rotating buffer sets on
+    # their own streams): one batch of 1000 chains leaves the SM schedulers
+    # ~60 % idle (7 latency-bound warps per SM); decomposition throughput
+    # saturates at ~14.6 K matrices/s with >= 2000 chains resident
+    # (profiles/r2_inflight.log), and 3 in flight also hide each batch's
+    # balance and sort behind the others' decompositions
+    depth = max(1, args.inflight)
+    sets = [synth.SynthBuffers(B, n, m, dev) for _ in range(depth)]
+    streams = [torch.cuda.Stream(dev) for _ in range(depth)]
     stream = torch.cuda.current_stream()
-    sh = ctypes.c_void_p(stream.cuda_stream)
     P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
 
     def make_events(k):
@@ -180,28 +187,38 @@ def bench_synth(args) -> dict:
                 e.record(stream)  # materialise the handles
         return evs
 
-    def step(ev_row=None):
+    def step(k, ev_row=None):
         arr = None
         if ev_row is not None:
             arr = (ctypes.c_void_p * 4)(*[e.cuda_event for e in ev_row[:4]])
-        rc = lib.fast_synth_batch_ev(P(D), B, n, m, ctypes.byref(bufs.struct), sh, arr)
+        st = streams[k % depth]
+        rc = lib.fast_synth_batch_ev(P(D), B, n, m, ctypes.byref(sets[k % depth].struct),
+                                     ctypes.c_void_p(st.cuda_stream), arr)
         _lib.check_rc(rc, "fast_synth_batch_ev")
 
-    for _ in range(args.warmup):
-        step()
+    def run_steps(K, evs=None):
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for st in streams:
+            st.wait_event(t0)
+        for k in range(K):
+            step(k, evs[k] if evs is not None else None)
+        for st in streams:
+            stream.wait_stream(st)
+        t1.record(stream)
+        return t0, t1
+
+    run_steps(max(args.warmup, depth))
     torch.cuda.synchronize()
-    status = bufs.status.cpu()
-    if int(status.abs().max()) != 0:
-        raise RuntimeError(f"synthesis failed on {int((status != 0).sum())} matrices")
+    for bufs in sets:
+        status = bufs.status.cpu()
+        if int(status.abs().max()) != 0:
+            raise RuntimeError(f"synthesis failed on {int((status != 0).sum())} matrices")
 
     evs = make_events(args.steps)
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     with ClockSampler(0) as clk:
-        t0.record(stream)
-        for k in range(args.steps):
-            step(evs[k])
-        t1.record(stream)
+        t0, t1 = run_steps(args.steps, evs)
         torch.cuda.synchronize()
     total_ms = t0.elapsed_time(t1)
     names = ("balance_kernel", "decompose_kernel", "sort_kernel")
@@ -211,6 +228,20 @@ def bench_synth(args) -> dict:
             per[k] += row[i].elapsed_time(row[i + 1])
     per = {k: v / args.steps for k, v in per.items()}
     ms_step = total_ms / args.steps
+    # one batch alone (nothing else in flight): the batch latency
+    torch.cuda.synchronize()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    lat_ev = make_events(1)[0]
+    a0.record(stream)
+    rc = lib.fast_synth_batch_ev(P(D), B, n, m, ctypes.byref(sets[0].struct),
+                                 ctypes.c_void_p(stream.cuda_stream),
+                                 (ctypes.c_void_p * 4)(*[e.cuda_event for e in lat_ev]))
+    _lib.check_rc(rc, "fast_synth_batch_ev")
+    a1.record(stream)
+    torch.cuda.synchronize()
+    batch_alone_ms = a0.elapsed_time(a1)
+    alone = {k: lat_ev[i].elapsed_time(lat_ev[i + 1]) for i, k in enumerate(names)}
+    bufs = sets[0]
     n_raw = bufs.n_raw.cpu().tolist()
     P_CHECK = min(64, B)
     dev_sub = device_subset(bufs, P_CHECK)
@@ -244,7 +275,8 @@ def bench_synth(args) -> dict:
     if not sm_hz:
         sm_hz = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
     peels = sum(n_raw) / len(n_raw)
-    roofline["decompose_cycles_per_peel"] = round(per["decompose_kernel"] * 1e-3 * sm_hz / peels, 1)
+    roofline["decompose_cycles_per_peel"] = round(alone["decompose_kernel"] * 1e-3 * sm_hz / peels,
+                                                  1)
 
     # ---- e2e: host (pinned) D -> device -> synth -> compact result -> host,
     # through the public host-buffer API (HostSynthPipeline: chunked, copies
@@ -257,7 +289,7 @@ def bench_synth(args) -> dict:
     if not args.no_e2e:
         Dh = torch.empty(D.shape, dtype=D.dtype, pin_memory=True)
         Dh.copy_(D)
-        del bufs
+        del bufs, sets
         torch.cuda.empty_cache()
         pipe = synth.HostSynthPipeline(B, n, m, chunk=args.e2e_chunk, depth=2)
         outs = [synth.HostSchedules(B, n, m), synth.HostSchedules(B, n, m)]
@@ -307,15 +339,16 @@ def bench_synth(args) -> dict:
         parity = {"parity_checked": k_chk, "against": "oracle/fast_oracle.c (pinned to tiersched "
                   "by tests/golden/headline_digests.json)", "paths": ["device", "e2e"] if hs is not None
                   else ["device"], "result": "bit-exact"}
-        cyc = per["decompose_kernel"] * 1e-3 * sm_hz / steps_mean
+        cyc = alone["decompose_kernel"] * 1e-3 * sm_hz / steps_mean
         roofline["chain"] = {
             "bound": "dependent shared-memory chain (Kuhn DFS)", "kernel": "decompose_kernel",
             "dfs_steps_per_matrix": round(steps_mean, 1),
             "steps_source": f"oracle DFS step counter on the {k_chk} checked matrices",
             "cycles_per_step": round(cyc, 1), "floor_cycles_per_step": DFS_STEP_FLOOR_CYCLES,
             "frac": round(DFS_STEP_FLOOR_CYCLES / cyc, 4),
-            "note": "whole-kernel cycles (all chains resident, kernel time = slowest chain) per DFS "
-                    "step; the floor is one step's dependent LDS->and->bfind->mad->selp chain"}
+            "note": "whole-kernel cycles of one batch alone (1000 chains resident, kernel time = "
+                    "slowest chain) per DFS step; the floor is one step's dependent "
+                    "LDS->and->bfind->mad->selp chain"}
 
     out = {
         "metric": "schedule synthesis throughput (FAST synthesize_fast, batch of 1000 traffic "
@@ -329,6 +362,9 @@ def bench_synth(args) -> dict:
                    "batch": B, "zipf_skew": args.skew, "total_bytes": args.total},
         "l2": "inputs larger than L2 (D batch = %.1f GB)" % (B * G * G * 8 / 1e9)
               if B * G * G * 8 > 126e6 else "inputs within L2",
+        "inflight_batches": depth,
+        "batch_alone_ms": round(batch_alone_ms, 3),
+        "batch_alone_kernel_ms": {k: round(v, 4) for k, v in alone.items()},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": 3 * args.steps, "clocks": clk.summary(),
         "stages_per_matrix_mean": round(peels, 1),
@@ -501,6 +537,8 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--nccl-only", action="store_true")
+    ap.add_argument("--inflight", type=int, default=3,
+                    help="config 5: batches in flight (rotating buffer sets / streams)")
     ap.add_argument("--experts", type=int, default=8)
     ap.add_argument("--e2e-chunk", type=int, default=125)
     args = ap.parse_args()
