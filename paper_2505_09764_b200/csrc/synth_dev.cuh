@@ -306,6 +306,26 @@ __device__ __forceinline__ void load_row64(const uint32_t* src, uint64_t& r0, ui
   "st.shared.u16 [pa], t;\n\t"                                        \
   "add.u32 pa, pa, 2;\n\t"
 
+// Seen update of the selected word.  The visited column's bit z0 is set in
+// ns (x = row & ns had it), so clearing it is a subtraction, which ptxas can
+// issue on the FMA pipe (IMAD.IADD) instead of the ALU pipe that the
+// decomposition saturates at high occupancy (ncu: ALU pipe 70 % of peak with
+// 3000 chains resident).  -DFAST_DFS_SEEN_AND: the and-not form.
+#ifdef FAST_DFS_SEEN_AND
+#define FAST_DFS_SEEN_UPDATE                                            \
+  "not.b32 z0, z0;\n\t"                                               \
+  "@p0 and.b32 ns0, ns0, z0;\n\t"                                     \
+  "@p1 and.b32 ns1, ns1, z0;\n\t"                                     \
+  "@p3 and.b32 ns2, ns2, z0;\n\t"                                     \
+  "@pz and.b32 ns3, ns3, z0;\n\t"
+#else
+#define FAST_DFS_SEEN_UPDATE                                            \
+  "@p0 sub.u32 ns0, ns0, z0;\n\t"                                     \
+  "@p1 sub.u32 ns1, ns1, z0;\n\t"                                     \
+  "@p3 sub.u32 ns2, ns2, z0;\n\t"                                     \
+  "@pz sub.u32 ns3, ns3, z0;\n\t"
+#endif
+
 // v2 step (default): select the first non-empty word (and its row
 // base) with predicates first, then ONE bfind on it -- one FLO per step
 // instead of four, and the seen update touches only the selected word.
@@ -334,11 +354,7 @@ __device__ __forceinline__ void load_row64(const uint32_t* src, uint64_t& r0, ui
   "or.b32 u, t, x2;\n\t"                                              \
   "setp.eq.u32 pz, u, 0;\n\t"                                         \
   "shr.u32 z0, hb, z0;\n\t"                                           \
-  "not.b32 z0, z0;\n\t"                                               \
-  "@p0 and.b32 ns0, ns0, z0;\n\t"                                     \
-  "@p1 and.b32 ns1, ns1, z0;\n\t"                                     \
-  "@p3 and.b32 ns2, ns2, z0;\n\t"                                     \
-  "@pz and.b32 ns3, ns3, z0;\n\t"                                     \
+  FAST_DFS_SEEN_UPDATE                                                  \
   "sub.u32 t, ad, bb0;\n\t"                                           \
   "st.shared.u16 [pa], t;\n\t"                                        \
   "add.u32 pa, pa, 2;\n\t"

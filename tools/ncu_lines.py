@@ -16,16 +16,26 @@ import sys
 import tempfile
 
 
-def sass_samples(report: str):
-    out = subprocess.run(["ncu", "-i", report, "--page", "source", "--csv", "--print-source", "sass"],
-                         capture_output=True, text=True).stdout
+def sass_samples(report: str, kernel: str = ""):
+    """[(offset, sass text, stall samples, instructions executed)] of the
+    first kernel matching `kernel` in the report."""
+    cmd = ["ncu", "-i", report, "--page", "source", "--csv", "--print-source", "sass"]
+    if kernel:
+        cmd += ["-k", f"regex:{kernel}"]
+    out = subprocess.run(cmd, capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr = rows[1]
+    h = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
+    hdr = rows[h]
     ia, isrc = hdr.index("Address"), hdr.index("Source")
     isamp = hdr.index("Warp Stall Sampling (All Samples)")
-    data = [(int(r[ia], 16), r[isrc].strip(), int(r[isamp] or 0)) for r in rows[2:]]
+    iexe = hdr.index("Instructions Executed")
+    data = []
+    for r in rows[h + 1:]:
+        if not r or not r[0].startswith("0x"):
+            break
+        data.append((int(r[ia], 16), r[isrc].strip(), int(r[isamp] or 0), int(r[iexe] or 0)))
     base = data[0][0]
-    return [(a - base, s, n) for a, s, n in data]
+    return [(a - base, s_, n, e) for a, s_, n, e in data]
 
 
 def line_table(lib: str, kernel: str):
@@ -54,18 +64,21 @@ def line_table(lib: str, kernel: str):
 def main():
     report, lib, kernel = sys.argv[1:4]
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 30
-    samples = sass_samples(report)
+    samples = sass_samples(report, kernel)
     tables = line_table(lib, kernel)
     # pick the function whose instruction count matches the ncu listing
     fn = min(tables, key=lambda k: abs(len(tables[k]) - len(samples)))
     tab = tables[fn]
-    agg = collections.Counter()
-    for off, _, n in samples:
+    agg, ins = collections.Counter(), collections.Counter()
+    for off, _, n, e in samples:
         agg[tab.get(off, "?")] += n
+        ins[tab.get(off, "?")] += e
     tot = sum(agg.values()) or 1
-    print(f"{fn}: {tot} samples")
+    itot = sum(ins.values()) or 1
+    print(f"{fn}: {tot} stall samples, {itot} warp instructions executed")
+    print(" samples%  instr%   line")
     for k, v in agg.most_common(top):
-        print(f"{100 * v / tot:6.2f}%  {k}")
+        print(f"{100 * v / tot:7.2f}% {100 * ins[k] / itot:7.2f}%  {k}")
 
 
 if __name__ == "__main__":
