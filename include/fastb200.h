@@ -328,6 +328,10 @@ int fast_comm_set_fused(fast_comm *c, int enable);
 int fast_comm_set_send_rows(fast_comm *c, const void *rows_base,
                             const int32_t *row_src, int64_t row_bytes,
                             int64_t n_rows);
+/* Programmatic dependent launch on the fast_alltoallv chain (gather ->
+ * synthesis -> plan -> exec: each kernel launches while its predecessor
+ * runs and waits for its memory with griddepcontrol.wait); on by default. */
+int fast_comm_set_pdl(fast_comm *c, int enable);
 /* Bytes the executor may read from the send side (the send buffer, or
  * n_rows * row_bytes of a row-mapped send); -1 (default) = unchecked.  Taken
  * at enqueue time.  An op reaching past it makes the exec copy nothing and

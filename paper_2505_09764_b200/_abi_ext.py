@@ -63,6 +63,7 @@ SIGNATURES: list[tuple[str, object, list]] = [
     ("fast_comm_set_fused", I, [V, I]),
     ("fast_comm_set_send_rows", I, [V, V, V, I64, I64]),
     ("fast_comm_set_send_capacity", I, [V, I64]),
+    ("fast_comm_set_pdl", I, [V, I]),
     ("fast_debug_copy", I, [V, V, I64, I, I64, I, V]),
     ("fast_debug_memcpy", I, [V, V, I64, V]),
     ("fast_comm_create_group", I, [I, I64, I64, ctypes.POINTER(V)]),

@@ -28,6 +28,7 @@
 #include <string.h>
 
 #include "fastb200.h"
+#include "launch.cuh"
 #include "plan_par.cuh"
 #include "synth_dev.cuh"
 
@@ -327,9 +328,11 @@ __global__ void bump_epoch_kernel(uint8_t* me) {
 
 __global__ void gather_demand_kernel(uint8_t* const* peers, const int64_t* row,
                                      int64_t epoch_in, int rank, int world,
-                                     int64_t demand_off) {
+                                     int64_t demand_off, int32_t* zero_status) {
   __shared__ int64_t s_epoch;
+  pdl_trigger();  // the synthesis kernels may launch; they wait for this grid
   if (threadIdx.x >= 32) return;
+  if (zero_status && threadIdx.x == 0) *zero_status = FAST_OK;  // the call's synthesis status
   uint8_t* me = peers[rank];
   if (threadIdx.x == 0) {
     volatile uint64_t* ep = reinterpret_cast<volatile uint64_t*>(me) + CTR_EPOCH;
@@ -427,6 +430,8 @@ __global__ void __launch_bounds__(kPlanThreads)
     fast_plan_kernel_dev(fastplan::PlanIn in, fastplan::PlanOut out, const int32_t* n_stages,
                          const int32_t* sched_status, int smem_ok) {
   extern __shared__ __align__(16) char psm[];
+  pdl_trigger();
+  pdl_wait();  // the schedule comes from the previous kernel of the chain
   PLAN_STAMP(9);
   if (*sched_status != FAST_OK) {
     if (threadIdx.x == 0) {
@@ -562,6 +567,7 @@ __global__ void __launch_bounds__(kExecThreads) exec_kernel(ExecArgs a, FusedArg
   __shared__ unsigned long long s_red[3];  // recv chunks expected, producer / redist bytes
   __shared__ int s_fail;
   extern __shared__ __align__(16) char fsm[];
+  pdl_wait();  // the plan comes from the previous kernel of the chain
   a.rank += blockIdx.y;
   a.send = a.sends[blockIdx.y];
   if (a.row_srcs[blockIdx.y]) {
@@ -761,6 +767,7 @@ struct fast_comm {
   uint32_t row_vec, row_magic;
   int row_l;
   int64_t send_cap;  // fast_comm_set_send_capacity (-1: unchecked)
+  int no_pdl;        // 1: plain launches on the alltoallv chain
 };
 
 static void set_rowmap(ExecArgs& a, const fast_comm* c) {
@@ -783,10 +790,25 @@ int64_t fast_plan_op_capacity(int n, int m) {
   return fastplan::plan_op_capacity(n, m, n * n - 2 * n + 2);
 }
 
+static int plan_compile_launch(const int64_t* D, const int64_t* send_self, int n, int m,
+                               const fast_sched_bufs* sched, int64_t recv_capacity,
+                               int64_t staging_capacity, int64_t chunk_bytes,
+                               const fast_plan* plan, void* stream, bool pdl);
+
 int fast_plan_compile(const int64_t* D, const int64_t* send_self, int n, int m,
                       const fast_sched_bufs* sched, int64_t recv_capacity,
                       int64_t staging_capacity, int64_t chunk_bytes, const fast_plan* plan,
                       void* stream) {
+  return plan_compile_launch(D, send_self, n, m, sched, recv_capacity, staging_capacity,
+                             chunk_bytes, plan, stream, false);
+}
+
+}  // extern "C"
+
+static int plan_compile_launch(const int64_t* D, const int64_t* send_self, int n, int m,
+                               const fast_sched_bufs* sched, int64_t recv_capacity,
+                               int64_t staging_capacity, int64_t chunk_bytes,
+                               const fast_plan* plan, void* stream, bool pdl) {
   if (!sched || !plan || n < 2 || m < 1 || m > FAST_MAX_GPUS_PER_SERVER) return FAST_EVALIDATION;
   fastplan::PlanIn in;
   in.n = n;
@@ -818,10 +840,14 @@ int fast_plan_compile(const int64_t* D, const int64_t* send_self, int n, int m,
       return FAST_ECUDA;
     plan_attr = smem;
   }
-  fast_plan_kernel_dev<<<1, kPlanThreads, smem_ok ? smem : 0, (cudaStream_t)stream>>>(
-      in, out, sched->n_stages, sched->status, smem_ok);
-  return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
+  return launch_k(fast_plan_kernel_dev, dim3(1), dim3(kPlanThreads), smem_ok ? smem : 0,
+                  (cudaStream_t)stream, pdl, in, out, (const int32_t*)sched->n_stages,
+                  (const int32_t*)sched->status, smem_ok) == cudaSuccess
+             ? FAST_OK
+             : FAST_ECUDA;
 }
+
+extern "C" {
 
 #ifdef FAST_PLAN_PROFILE
 int fast_debug_plan_prof(long long* out16) {
@@ -956,7 +982,7 @@ int64_t fast_comm_staging_capacity(const fast_comm* c) { return c ? c->staging_b
 int fast_gather_demand(fast_comm* c, const int64_t* row, int64_t epoch, void* stream) {
   if (!c || !c->opened || !row || epoch < 1) return FAST_EVALIDATION;
   gather_demand_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(c->peers_dev, row, epoch, c->rank,
-                                                           c->world, c->demand_off);
+                                                           c->world, c->demand_off, nullptr);
   return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
 }
 
@@ -977,7 +1003,7 @@ static int max_resident_blocks() {
 
 static int exec_launch(fast_comm* c, const fast_plan* plan, const void* send, int64_t epoch,
                        int blocks, int64_t chunk_bytes, int64_t* timeline_ns, void* stream,
-                       int skip_barrier);
+                       int skip_barrier, bool pdl = false);
 
 int fast_exec(fast_comm* c, const fast_plan* plan, const void* send, int64_t epoch, int blocks,
               int64_t chunk_bytes, int64_t* timeline_ns, void* stream) {
@@ -986,7 +1012,7 @@ int fast_exec(fast_comm* c, const fast_plan* plan, const void* send, int64_t epo
 
 static int exec_launch(fast_comm* c, const fast_plan* plan, const void* send, int64_t epoch,
                        int blocks, int64_t chunk_bytes, int64_t* timeline_ns, void* stream,
-                       int skip_barrier) {
+                       int skip_barrier, bool pdl) {
   // epoch 0: the kernel reads this call's epoch from the device counter
   if (!c || !c->opened || !plan || epoch < 0 || blocks < 1 || chunk_bytes < 16)
     return FAST_EVALIDATION;
@@ -1012,8 +1038,10 @@ static int exec_launch(fast_comm* c, const fast_plan* plan, const void* send, in
   a.staging_cap = c->staging_bytes;
   FusedArgs f;
   memset(&f, 0, sizeof(f));
-  exec_kernel<false><<<blocks, kExecThreads, 0, (cudaStream_t)stream>>>(a, f);
-  return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
+  return launch_k(exec_kernel<false>, dim3(blocks), dim3(kExecThreads), 0, (cudaStream_t)stream,
+                  pdl, a, f) == cudaSuccess
+             ? FAST_OK
+             : FAST_ECUDA;
 }
 
 int fast_comm_create_group(int world, int64_t recv_bytes, int64_t staging_bytes,
@@ -1184,18 +1212,28 @@ int fast_alltoallv(fast_comm* c, const void* send, const int64_t* counts, int n,
                         (cudaStream_t)stream);
   // device-side epoch (gather_demand_kernel bumps it): every argument below
   // is call-invariant, so the whole call can be captured in a CUDA graph
+  // the gather also zeroes the call's synthesis status, so no memset node
+  // breaks the programmatic (PDL) chain gather -> synthesis -> plan -> exec
   gather_demand_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(c->peers_dev, counts, 0, c->rank,
-                                                           c->world, c->demand_off);
+                                                           c->world, c->demand_off,
+                                                           sched->status);
   if (cudaGetLastError() != cudaSuccess) return FAST_ECUDA;
   c->epoch += 1;
   int rc;
+  const bool pdl = !c->no_pdl;
   int64_t* D = fast_comm_demand_ptr(c, 0);
-  rc = fast_synth_batch(D, 1, n, m, sched, stream);
+  rc = fast_synth_batch_chain(D, 1, n, m, sched, (cudaStream_t)stream, pdl);
   if (rc != FAST_OK) return rc;
-  rc = fast_plan_compile(D, D + (int64_t)c->world * c->world, n, m, sched, c->recv_bytes,
-                         c->staging_bytes, chunk_bytes, plan, stream);
+  rc = plan_compile_launch(D, D + (int64_t)c->world * c->world, n, m, sched, c->recv_bytes,
+                           c->staging_bytes, chunk_bytes, plan, stream, pdl);
   if (rc != FAST_OK) return rc;
-  return exec_launch(c, plan, send, 0, blocks, chunk_bytes, timeline_ns, stream, 1);
+  return exec_launch(c, plan, send, 0, blocks, chunk_bytes, timeline_ns, stream, 1, pdl);
+}
+
+int fast_comm_set_pdl(fast_comm* c, int enable) {
+  if (!c) return FAST_EVALIDATION;
+  c->no_pdl = enable ? 0 : 1;
+  return FAST_OK;
 }
 
 int fast_comm_set_send_capacity(fast_comm* c, int64_t bytes) {

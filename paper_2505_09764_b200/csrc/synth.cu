@@ -26,6 +26,7 @@
 #include <stdint.h>
 
 #include "fastb200.h"
+#include "launch.cuh"
 
 namespace {
 
@@ -109,6 +110,8 @@ __global__ void __launch_bounds__(kBalThreads)
     balance_kernel(const int64_t* __restrict__ D, const int n, const int m_rt,
                    const int J, fast_sched_bufs out) {
   extern __shared__ int64_t sm[];
+  pdl_trigger();
+  pdl_wait();  // D comes from the previous kernel of an alltoallv chain
   const int m = M ? M : m_rt;
   const int b = blockIdx.z, i = blockIdx.x, j0 = blockIdx.y * J;
   const int Jc = min(J, n - j0);
@@ -323,6 +326,8 @@ __global__ void __launch_bounds__(kDecWarps * 32)
                      const int n, const int mode, const int check_total,
                      fast_sched_bufs out) {
   extern __shared__ __align__(16) char dsm[];
+  pdl_trigger();
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x * kDecWarps + warp;
   if (b >= B) return;
@@ -370,6 +375,8 @@ __global__ void __launch_bounds__(kSortThreads)
     sort_kernel(const int n, fast_sched_bufs out) {
   extern __shared__ __align__(16) unsigned long long sk[];
   __shared__ unsigned long long s_max;
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.x;
   const int K = stage_cap(n);
   if (out.status[b] != FAST_OK) return;
@@ -621,7 +628,7 @@ int launch_balance_tma(const int64_t* D, int B, int n, const fast_sched_bufs* ou
 #endif  // FAST_BAL_TMA
 
 int launch_balance(const int64_t* D, int B, int n, int m,
-                   const fast_sched_bufs* out, cudaStream_t s) {
+                   const fast_sched_bufs* out, cudaStream_t s, bool pdl = false) {
 #ifdef FAST_BAL_TMA
   // opt-in: the TMA-fed per-thread pipeline.  Measured 2.3x SLOWER than the
   // staged kernel below (13.0 vs 5.6 ms at n=128 x 8, B=1000;
@@ -648,7 +655,9 @@ int launch_balance(const int64_t* D, int B, int n, int m,
                                (int)smem);                                   \
       if (e != cudaSuccess) return FAST_ECUDA;                               \
     }                                                                        \
-    balance_kernel<MV><<<grid, kBalThreads, smem, s>>>(D, n, m, J, *out);    \
+    e = launch_k(balance_kernel<MV>, grid, dim3(kBalThreads), smem, s, pdl,   \
+                 D, n, m, J, *out);                                          \
+    if (e != cudaSuccess) return FAST_ECUDA;                                 \
     break;
   switch (m) {
     FAST_BAL_CASE(1)
@@ -661,7 +670,8 @@ int launch_balance(const int64_t* D, int B, int n, int m,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem);
       if (smem > 48 * 1024 && e != cudaSuccess) return FAST_ECUDA;
-      balance_kernel<0><<<grid, kBalThreads, smem, s>>>(D, n, m, J, *out);
+      e = launch_k(balance_kernel<0>, grid, dim3(kBalThreads), smem, s, pdl, D, n, m, J, *out);
+      if (e != cudaSuccess) return FAST_ECUDA;
   }
 #undef FAST_BAL_CASE
   return check(cudaGetLastError());
@@ -669,7 +679,7 @@ int launch_balance(const int64_t* D, int B, int n, int m,
 
 template <int NW, bool WB>
 int launch_decompose_wb(const int64_t* S, int B, int n, int mode, int check_total,
-                        const fast_sched_bufs* out, cudaStream_t s) {
+                        const fast_sched_bufs* out, cudaStream_t s, bool pdl) {
   const size_t smem = dec_smem_bytes_t<NW>(n) * kDecWarps;
   static size_t granted = 0;  // per template instance
   if (smem > 48 * 1024 && smem > granted) {
@@ -679,26 +689,29 @@ int launch_decompose_wb(const int64_t* S, int B, int n, int mode, int check_tota
     granted = smem;
   }
   const int grid = (B + kDecWarps - 1) / kDecWarps;
-  decompose_kernel<NW, WB><<<grid, kDecWarps * 32, smem, s>>>(S, B, n, mode, check_total, *out);
-  return FAST_OK;
+  return launch_k(decompose_kernel<NW, WB>, dim3(grid), dim3(kDecWarps * 32), smem, s, pdl, S, B,
+                  n, mode, check_total, *out) == cudaSuccess
+             ? FAST_OK
+             : FAST_ECUDA;
 }
 
 template <int NW>
 int launch_decompose_t(const int64_t* S, int B, int n, int mode, int check_total,
-                       const fast_sched_bufs* out, cudaStream_t s) {
-  return out->stage_bytes ? launch_decompose_wb<NW, true>(S, B, n, mode, check_total, out, s)
-                          : launch_decompose_wb<NW, false>(S, B, n, mode, check_total, out, s);
+                       const fast_sched_bufs* out, cudaStream_t s, bool pdl) {
+  return out->stage_bytes
+             ? launch_decompose_wb<NW, true>(S, B, n, mode, check_total, out, s, pdl)
+             : launch_decompose_wb<NW, false>(S, B, n, mode, check_total, out, s, pdl);
 }
 
 int launch_decompose(const int64_t* S, int B, int n, int mode, int check_total,
                      const fast_sched_bufs* out, cudaStream_t s,
-                     cudaEvent_t after_decompose = nullptr) {
+                     cudaEvent_t after_decompose = nullptr, bool pdl = false) {
   int rc;
   switch ((n + 31) / 32) {
-    case 1: rc = launch_decompose_t<1>(S, B, n, mode, check_total, out, s); break;
-    case 2: rc = launch_decompose_t<2>(S, B, n, mode, check_total, out, s); break;
-    case 3: rc = launch_decompose_t<3>(S, B, n, mode, check_total, out, s); break;
-    default: rc = launch_decompose_t<4>(S, B, n, mode, check_total, out, s); break;
+    case 1: rc = launch_decompose_t<1>(S, B, n, mode, check_total, out, s, pdl); break;
+    case 2: rc = launch_decompose_t<2>(S, B, n, mode, check_total, out, s, pdl); break;
+    case 3: rc = launch_decompose_t<3>(S, B, n, mode, check_total, out, s, pdl); break;
+    default: rc = launch_decompose_t<4>(S, B, n, mode, check_total, out, s, pdl); break;
   }
   if (rc != FAST_OK) return rc;
   if (cudaGetLastError() != cudaSuccess) return FAST_ECUDA;
@@ -715,8 +728,7 @@ int launch_decompose(const int64_t* S, int B, int n, int mode, int check_total,
   }
   int threads = (stage_cap(n) / 2 + 31) & ~31;
   threads = threads < 32 ? 32 : (threads > kSortThreads ? kSortThreads : threads);
-  sort_kernel<<<B, threads, ssmem, s>>>(n, *out);
-  return check(cudaGetLastError());
+  return check(launch_k(sort_kernel, dim3(B), dim3(threads), ssmem, s, pdl, n, *out));
 }
 
 bool bad_shape(int B, int n, int m) {
@@ -815,5 +827,18 @@ int fast_synth_batch(const int64_t* D, int B, int n, int m,
                      const fast_sched_bufs* out, void* stream) {
   return fast_synth_batch_ev(D, B, n, m, out, stream, nullptr);
 }
+
+}  // extern "C"
+
+int fast_synth_batch_chain(const int64_t* D, int B, int n, int m, const fast_sched_bufs* out,
+                           cudaStream_t s, bool pdl) {
+  if (bad_shape(B, n, m) || !out) return FAST_EVALIDATION;
+  if (B == 0) return FAST_OK;
+  int rc = launch_balance(D, B, n, m, out, s, pdl);
+  if (rc != FAST_OK) return rc;
+  return launch_decompose(out->server, B, n, FAST_DEC_SERVER, 1, out, s, nullptr, pdl);
+}
+
+extern "C" {
 
 }  // extern "C"

@@ -201,6 +201,12 @@ class FastComm:
         _lib.check_rc(_lib.load().fast_comm_set_fused(self._ptr, 1 if enable else 0), "set_fused")
         self._fused = bool(enable)
 
+    def set_pdl(self, enable: bool) -> None:
+        """Programmatic dependent launch on the per-call kernel chain (on by
+        default); cached call graphs are re-captured."""
+        _lib.check_rc(_lib.load().fast_comm_set_pdl(self._ptr, 1 if enable else 0), "set_pdl")
+        self._graphs.clear()
+
     def close(self) -> None:
         if getattr(self, "_ptr", None):
             _lib.load().fast_comm_destroy(self._ptr)
