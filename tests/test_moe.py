@@ -198,3 +198,89 @@ def test_moe_combine_group_mode_matches_oracle():
         got = outs[s].cpu().view(torch.int16).numpy().view(np.uint16)
         assert np.array_equal(got, want[s]), s
     group.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k,L", [(1, 2), (4, 2), (2, 3)])
+def test_router_topk_experts_per_rank_group_mode(k, L):
+    """The router's top-k ids (any k in 1/2/4/8, duplicates allowed) with
+    E = L * world experts, L per rank: expert inputs and the weighted
+    combine are bit-exact vs the numpy oracle (group mode, 2x2)."""
+    from paper_2505_09764_b200 import Topology
+    from paper_2505_09764_b200.executor import GroupComm, GroupRank
+    from paper_2505_09764_b200.moe import MoEDispatch
+
+    G, T, H = 4, 1200, 256
+    E = G * L
+    RB = 2 * H
+    gen = torch.Generator().manual_seed(k * 10 + L)
+    toks = [torch.randn(T, H, generator=gen).to(torch.bfloat16) for _ in range(G)]
+    toks_u8 = [t.view(torch.uint8).numpy().reshape(T, RB) for t in toks]
+    toks_u16 = [t.view(torch.int16).numpy().view(np.uint16) for t in toks]
+    topks = [np.random.default_rng(70 + s).integers(0, E, (T, k)).astype(np.int32)
+             for s in range(G)]
+    weights = [torch.rand(T, k, generator=gen, dtype=torch.float32) for _ in range(G)]
+    cap = k * T * RB * 4
+    group = GroupComm(Topology(2, 2), recv_bytes=cap, staging_bytes=cap, blocks=8)
+    ds = []
+    for s in range(G):
+        d = MoEDispatch(GroupRank(group, s), T, RB, k=k, num_experts=E)
+        d.route(topk=torch.from_numpy(topks[s]).cuda())
+        d.pack(toks[s].cuda())
+        ds.append(d)
+    torch.cuda.synchronize()
+    for s, d in enumerate(ds):
+        counts, _, _ = moe_oracle.route(topks[s], E)
+        assert np.array_equal(d.counts.cpu().numpy(), counts), s
+        dr = d.demand_row.cpu().numpy()
+        assert np.array_equal(dr, counts.reshape(G, L).sum(1) * RB), s
+    Dfull = torch.stack([d.demand_row for d in ds])
+    selfb = torch.diagonal(Dfull).clone()
+    D = Dfull.clone()
+    D.fill_diagonal_(0)
+    recvs = group.alltoallv([d.send for d in ds], D, self_bytes=selfb)
+    for s, d in enumerate(ds):
+        d.unpack(D=D, self_sizes=selfb, recv=recvs[s])
+    torch.cuda.synchronize()
+    group.check()
+    want = moe_oracle.expert_inputs(toks_u8, topks, E, L)
+    expert_out = []
+    for h, d in enumerate(ds):
+        n_in = want[h].size
+        assert np.array_equal(recvs[h][:n_in].cpu().numpy().reshape(-1, RB), want[h]), h
+        d.remember_forward(D, selfb)
+        x = recvs[h][:n_in].view(torch.bfloat16) * (2.0 ** h)  # rank h's experts (exact)
+        buf = torch.empty(cap, dtype=torch.uint8, device="cuda")
+        buf[:n_in].copy_(x.view(torch.uint8))
+        expert_out.append(buf)
+    comb = group.alltoallv(expert_out, D.t().contiguous(), self_bytes=selfb)
+    outs = []
+    for s, d in enumerate(ds):
+        o = torch.empty(T, H, dtype=torch.bfloat16, device="cuda")
+        d.combine_rows(comb[s], expert_out[s], weights[s].cuda(), o)
+        outs.append(o)
+    torch.cuda.synchronize()
+    group.check()
+    wantc = moe_oracle.combine(toks_u16, topks, [w.numpy() for w in weights],
+                               lambda e: 2.0 ** (e // L))
+    for s in range(G):
+        assert np.array_equal(outs[s].cpu().view(torch.int16).numpy().view(np.uint16),
+                              wantc[s]), s
+    group.close()
+
+
+@pytest.mark.gpu
+def test_router_topk_invalid_ids_fail_loudly():
+    """An expert id outside [0, E) poisons the demand row (-1): the
+    alltoallv's synthesis rejects the matrix instead of dropping tokens."""
+    from paper_2505_09764_b200 import Topology
+    from paper_2505_09764_b200.executor import GroupComm, GroupRank
+    from paper_2505_09764_b200.moe import MoEDispatch
+
+    group = GroupComm(Topology(2, 1), recv_bytes=1 << 20, staging_bytes=1 << 20, blocks=4)
+    d = MoEDispatch(GroupRank(group, 0), 64, 256, k=2, num_experts=4)
+    tk = np.random.default_rng(0).integers(0, 4, (64, 2)).astype(np.int32)
+    tk[5, 1] = 9
+    d.route(topk=torch.from_numpy(tk).cuda())
+    assert (d.demand_row.cpu().numpy() == -1).all()
+    group.close()
