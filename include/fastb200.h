@@ -4,7 +4,7 @@
  * Plain pointers and sizes only (no torch types).  All device pointers are
  * caller-owned; every call is stream-ordered on `stream` (a cudaStream_t
  * passed as void*), reentrant, and keeps no hidden global state except the
- * communicator objects returned by fast_comm_init.
+ * communicator objects returned by fast_comm_create.
  *
  * Return codes mirror the reference's error classes (tiersched
  * model.py:29-34) and CLI exit codes (cli.py:420-433):

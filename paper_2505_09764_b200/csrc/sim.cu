@@ -31,7 +31,20 @@ namespace {
 constexpr int kSimThreads = 256;
 constexpr int kSimWarps = kSimThreads / 32;
 constexpr int kSimMaxM = 64;
-constexpr int kSimGridMax = 4 * 148;
+// CTAs per launch: 4 per SM of the current device (persistent loop over
+// schedules); the workspace is sized with the same figure
+inline int sim_grid_max() {
+  static int g = 0;
+  if (!g) {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        sms <= 0)
+      sms = 148;  // no device (host-side sizing only): B200
+    g = 4 * sms;
+  }
+  return g;
+}
 constexpr size_t kSimWsBudget = (size_t)2 << 30;
 
 __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -44,7 +57,8 @@ __host__ __device__ inline size_t sim_cta_bytes(int n, int m, int K) {
 
 inline int sim_grid(int B, int n, int m, int K) {
   const size_t per = sim_cta_bytes(n, m, K);
-  int g = B < kSimGridMax ? B : kSimGridMax;
+  const int gmax = sim_grid_max();
+  int g = B < gmax ? B : gmax;
   const size_t cap = kSimWsBudget / per;
   if ((size_t)g > cap) g = cap > 0 ? (int)cap : 1;
   return g > 0 ? g : 1;
