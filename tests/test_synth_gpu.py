@@ -75,7 +75,8 @@ def test_gpu_matches_every_golden_decomposition(golden_decompositions):
         assert [[st.weight, [list(e) for e in st.edges]] for st in again] == rec["raw"]
 
 
-@pytest.mark.parametrize("n,B", [(16, 64), (32, 16), (64, 4), (128, 2), (64, 40), (128, 17)])
+@pytest.mark.parametrize("n,B", [(16, 64), (32, 16), (64, 4), (128, 2), (64, 40), (128, 17),
+                                 (128, 24), (80, 30), (100, 41)])
 def test_gpu_matches_oracle_config5_shapes(n, B):
     m = 8
     G = n * m
