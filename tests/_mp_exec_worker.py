@@ -42,7 +42,14 @@ def main() -> int:
     # ranks on one device, so the bootstrap is gloo and the all_to_all_single
     # comparisons use the CPU oracle instead of NCCL.
     one_gpu = os.environ.get("FAST_MP_ONE_GPU") == "1"
-    torch.cuda.set_device(0 if one_gpu else int(os.environ.get("LOCAL_RANK", rank)))
+    # FAST_MP_GPUS=k: rank r on cuda:(r % k) -- more ranks than GPUs (e.g. the
+    # 8-rank 2x4 / 4x2 partitions on a 4-GPU box); gloo bootstrap as above
+    share = int(os.environ.get("FAST_MP_GPUS", "0"))
+    if share:
+        one_gpu = True  # same host-side comparisons (no NCCL with shared devices)
+        torch.cuda.set_device(rank % share)
+    else:
+        torch.cuda.set_device(0 if one_gpu else int(os.environ.get("LOCAL_RANK", rank)))
     dist.init_process_group("gloo" if one_gpu else "nccl")
     ok = True
     for (n, m) in partitions(world):
@@ -50,6 +57,7 @@ def main() -> int:
                  workloads.gen_uniform(6, Topology(n, m), 300_001).sizes,
                  workloads.gen_adversarial(Topology(n, m), 1_234_567).sizes]
         cap = max(int(max(c.sum(0).max(), c.sum(1).max())) for c in cases) + 4096
+        cap = max(cap, world * 64 * 4096 * 4 + 4096)  # the all_to_all_fast cases (fp32 rows)
         comm = FastComm(Topology(n, m), recv_bytes=cap, staging_bytes=2 * cap + (1 << 20),
                         blocks=16, chunk_bytes=128 * 1024)
         for ci, D in enumerate(cases + cases):

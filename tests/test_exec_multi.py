@@ -46,3 +46,12 @@ def test_fastcomm_multiprocess_parity():
 def test_fastcomm_multiprocess_one_gpu(nproc):
     """Separate processes on ONE device: IPC mappings + system-scope flags."""
     _run(nproc, {"FAST_MP_ONE_GPU": "1"}, 29540 + nproc)
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs")
+def test_fastcomm_eight_ranks_shared_gpus():
+    """8 ranks (the 2x4 and 4x2 partitions of BASELINE configs 2-4) on the
+    GPUs available, two or more processes per device: cross-GPU IPC
+    mappings and same-GPU ones in one communicator."""
+    _run(8, {"FAST_MP_GPUS": str(min(4, torch.cuda.device_count()))}, 29560)
