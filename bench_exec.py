@@ -122,6 +122,27 @@ def peer_copy_peaks(comm, rank: int, nbytes: int) -> dict | None:
     return res
 
 
+def timeline_vs_model(D: np.ndarray, n: int, m: int, tls: list, peaks_run) -> dict:
+    """Measured Timeline (rank 0 and the slowest rank; seconds) beside
+    simulate_fast's model of the same schedule (simulate.py:107-193) with both
+    tiers at the in-run SM-store peer peak (one NVLink tier)."""
+    from paper_2505_09764_b200 import DemandMatrix, Topology, simulate_fast, synthesize_fast
+
+    bw = (peaks_run["GBps"]["sm_copy"] if peaks_run else PEER_GBS) * 1e9
+    t = Topology(n, m, bw, bw)
+    sch = synthesize_fast(DemandMatrix(n, m, np.asarray(D, np.int64)), t)
+    model = simulate_fast(sch.plan, list(sch.stages), t).to_json_dict()
+    slow = max(range(len(tls)), key=lambda r: tls[r]["total"])
+    r6 = lambda d: {k: (round(v * 1e6, 2) if isinstance(v, float) else  # noqa: E731
+                        [round(x * 1e6, 2) for x in v]) for k, v in d.items()}
+    return {"unit": "us", "measured_rank0": r6(tls[0]), "measured_slowest_rank": slow,
+            "measured_slowest": r6(tls[slow]), "model_simulate_fast": r6(model),
+            "model_bandwidth_GBps": round(bw / 1e9, 1),
+            "note": "measured: device %globaltimer windows of one call (phase durations; total = "
+                    "exec start to the rank's last send and arrival); model: the reference's "
+                    "pipelined cost model, both tiers at the measured SM-store peer peak"}
+
+
 def fast_wire_bytes(ops: np.ndarray, G: int) -> tuple[int, int]:
     eg = np.zeros(G, np.int64)
     ing = np.zeros(G, np.int64)
@@ -228,6 +249,14 @@ def run(args, workload: str) -> dict | None:
     nvl_all = [None] * world
     dist.all_gather_object(nvl_all, nvl_rank)
     peaks_run = peer_copy_peaks(comm, rank, min(comm.recv_bytes - 4096, 128 << 20))
+    # measured per-phase Timeline of one call (device %globaltimer windows),
+    # every rank, next to the reference's analytical model of the same schedule
+    comm.alltoallv(send, row, record_timeline=True)
+    torch.cuda.synchronize()
+    comm.check()
+    tl = comm.measured_timeline()
+    tls = [None] * world
+    dist.all_gather_object(tls, tl.to_json_dict())
 
     # NCCL all_to_all_single on the identical traffic (practical B200 bar)
     ins, outs = D[rank].tolist(), D[:, rank].tolist()
@@ -332,6 +361,10 @@ def run(args, workload: str) -> dict | None:
                 "per_rank": per,
                 "max_rx_GBps_of_900": round(max(p["rx_GBps"] for p in per) / NVLINK_NOMINAL, 4),
                 "wire_bytes_vs_plan": round(max(x[1] for x in nvl_all) / max(fast_in, 1), 4)}
+        try:
+            res["timeline"] = timeline_vs_model(D, n, m, tls, peaks_run)
+        except Exception as exc:  # pragma: no cover - reported, not fatal
+            res["timeline"] = {"error": repr(exc)[:200]}
         if peaks_run:
             pk = peaks_run["GBps"]["sm_copy"]
             res["roofline"]["frac_of_in_run_sm_peak"] = round(
