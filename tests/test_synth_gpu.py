@@ -76,7 +76,7 @@ def test_gpu_matches_every_golden_decomposition(golden_decompositions):
 
 
 @pytest.mark.parametrize("n,B", [(16, 64), (32, 16), (64, 4), (128, 2), (64, 40), (128, 17),
-                                 (128, 24), (80, 30), (100, 41)])
+                                 (128, 24), (80, 30), (100, 41), (128, 40)])
 def test_gpu_matches_oracle_config5_shapes(n, B):
     m = 8
     G = n * m
