@@ -178,123 +178,6 @@ __global__ void __launch_bounds__(kBalThreads)
 }
 
 
-// ---------------------------------------------------------------------------
-// balance_pipe_kernel: balance_kernel as a persistent, double-buffered
-// pipeline.  Each CTA loops over (matrix, server row, destination block)
-// strips; while its threads balance strip k in one buffer, the 8-byte
-// cp.async copies of strip k+1 fill the other (same padded tile-major layout
-// as balance_kernel, so the per-tile greedy stays bank-conflict-free), so
-// the HBM stream does not stop during the sequential greedy.
-template <int M>
-__device__ __forceinline__ void strip_async_load(int64_t* __restrict__ sm,
-                                                 const int64_t* __restrict__ g_in,
-                                                 const int64_t G, const int Jc) {
-  constexpr int TS = M * M + 1;
-  const int cols = Jc * M;
-  for (int r = 0; r < M; ++r) {
-    const int64_t* row = g_in + (int64_t)r * G;
-    for (int col = threadIdx.x; col < cols; col += blockDim.x) {
-      const int jj = col / M, c = col - jj * M;
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                       (uint32_t)__cvta_generic_to_shared(sm + jj * TS + r * M + c)),
-                   "l"(row + col)
-                   : "memory");
-    }
-  }
-}
-
-template <int M>
-__global__ void __launch_bounds__(kBalThreads)
-    balance_pipe_kernel(const int64_t* __restrict__ D, const int n, const int B, const int J,
-                        fast_sched_bufs out) {
-  extern __shared__ int64_t sm[];
-  pdl_trigger();
-  pdl_wait();
-  constexpr int TS = M * M + 1;
-  const int64_t G = (int64_t)n * M;
-  const int nj = (n + J - 1) / J;
-  const int64_t items = (int64_t)B * n * nj;
-  int64_t* buf[2] = {sm, sm + (int64_t)J * TS};
-  auto decode = [&](int64_t it, int& b, int& i, int& j0) {
-    b = (int)(it / ((int64_t)n * nj));
-    const int64_t r = it - (int64_t)b * n * nj;
-    i = (int)(r / nj);
-    j0 = (int)(r - (int64_t)i * nj) * J;
-  };
-  int64_t it = blockIdx.x;
-  if (it < items) {
-    int b, i, j0;
-    decode(it, b, i, j0);
-    strip_async_load<M>(buf[0], D + (int64_t)b * G * G + (int64_t)i * M * G + (int64_t)j0 * M,
-                        G, min(J, n - j0));
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  for (int k = 0; it < items; it += gridDim.x, k ^= 1) {
-    const int64_t nxt = it + gridDim.x;
-    if (nxt < items) {
-      int b, i, j0;
-      decode(nxt, b, i, j0);
-      strip_async_load<M>(buf[k ^ 1],
-                          D + (int64_t)b * G * G + (int64_t)i * M * G + (int64_t)j0 * M, G,
-                          min(J, n - j0));
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
-    __syncthreads();
-    int b, i, j0;
-    decode(it, b, i, j0);
-    const int Jc = min(J, n - j0);
-    int64_t* t0 = buf[k];
-    if (threadIdx.x < Jc) {
-      const int jj = threadIdx.x, j = j0 + jj;
-      int64_t* t = t0 + jj * TS;
-      int32_t* st = out.status + b;
-      int64_t rs[M];
-      bool bad = false;
-      int64_t s = 0, tp = 0;
-#pragma unroll
-      for (int p = 0; p < M; ++p) {
-        int64_t r = 0;
-#pragma unroll
-        for (int q = 0; q < M; ++q) {
-          const int64_t v = t[p * M + q];
-          r += v;
-          if (v < 0) { bad = true; continue; }
-          if (i == j && p == q && v != 0) bad = true;
-          s = sat_add(s, v);
-        }
-        rs[p] = r;
-        tp += r;
-      }
-      out.server[(int64_t)b * n * n + i * n + j] = s;
-      if (bad) {
-        raise_status(st, FAST_EVALIDATION);
-      } else if (i != j) {
-        const int T = n * (n - 1);
-        const int slots = M > 1 ? M - 1 : 1;
-        const int tidx = i * (n - 1) + (j < i ? j : j - 1);
-        fast_move* mv = out.moves + ((int64_t)b * T + tidx) * slots;
-        uint64_t mk = 0;
-        int nm = balance_tile<M>(t, M, mv, slots, rs, &mk);
-        if (out.tile_mask) out.tile_mask[(int64_t)b * T + tidx] = mk;
-        if (nm < 0) {
-          raise_status(st, FAST_EINVARIANT);
-          nm = 0;
-        } else if (tp != s) {
-          raise_status(st, FAST_EINVARIANT);
-        }
-        out.move_count[(int64_t)b * T + tidx] = nm;
-      }
-    }
-    __syncthreads();
-    strip_rows<M>(t0, nullptr,
-                  out.balanced + (int64_t)b * G * G + (int64_t)i * M * G + (int64_t)j0 * M, M, G,
-                  Jc, false);
-    __syncthreads();  // buf[k] is refilled by the load issued next iteration
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-}
-
 #ifdef FAST_BAL_TMA
 // ---------------------------------------------------------------------------
 // balance_tma_kernel (opt-in, -DFAST_BAL_TMA; slower, see launch_balance):
@@ -744,41 +627,8 @@ int launch_balance_tma(const int64_t* D, int B, int n, const fast_sched_bufs* ou
 
 #endif  // FAST_BAL_TMA
 
-template <int M>
-int launch_balance_pipe(const int64_t* D, int B, int n, const fast_sched_bufs* out,
-                        cudaStream_t s, bool pdl) {
-  const size_t tile_bytes = (size_t)(M * M + 1) * 8;
-  int J = (int)((FAST_BAL_STRIP_KB * 1024) / tile_bytes);
-  if (J > 64) J = 64;
-  if (J > n) J = n;
-  const size_t smem = 2 * (size_t)J * tile_bytes;
-  static int grid = 0;
-  if (!grid) {
-    if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(balance_pipe_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-      return FAST_ECUDA;
-    int dev = 0, sms = 0, per_sm = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, balance_pipe_kernel<M>,
-                                                      kBalThreads, smem) != cudaSuccess)
-      return FAST_ECUDA;
-    grid = sms * (per_sm > 0 ? per_sm : 1);
-  }
-  const int64_t items = (int64_t)B * n * ((n + J - 1) / J);
-  const int g = items < grid ? (int)items : grid;
-  return check(launch_k(balance_pipe_kernel<M>, dim3(g), dim3(kBalThreads), smem, s, pdl, D, n, B,
-                        J, *out));
-}
-
 int launch_balance(const int64_t* D, int B, int n, int m,
                    const fast_sched_bufs* out, cudaStream_t s, bool pdl = false) {
-#ifndef FAST_BAL_NO_PIPE
-  // large batches: the persistent double-buffered pipeline
-  if (m == 8 && (int64_t)B * n * n >= (int64_t)64 * 148 * 64)
-    return launch_balance_pipe<8>(D, B, n, out, s, pdl);
-#endif
 #ifdef FAST_BAL_TMA
   // opt-in: the TMA-fed per-thread pipeline.  Measured 2.3x SLOWER than the
   // staged kernel below (13.0 vs 5.6 ms at n=128 x 8, B=1000;
