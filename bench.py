@@ -252,21 +252,10 @@ def bench_synth(args) -> dict:
     alg = {"balance_kernel": 16 * G * G * B,
            "decompose_kernel": algorithmic_bytes_decompose(n, n_raw),
            "sort_kernel": int(sum(8 * 2 * k for k in n_raw))}
-    dom = max(per, key=per.get)
-    achieved = alg[dom] / (per[dom] * 1e-3) / 1e9
     traffic = None
     tf = os.path.join(REPO, "profiles", "ncu_traffic.json")
     if os.path.exists(tf):
-        key = f"{dom}/n{n}_m{m}_B{B}"
-        traffic = json.load(open(tf)).get(key)
-    roofline = {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved / hbm, 5), "traffic": traffic, "kernel": dom,
-                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                "kernel_ms": {k: round(v, 4) for k, v in per.items()},
-                "balance_kernel_gbs": round(alg["balance_kernel"] / (per["balance_kernel"] * 1e-3) / 1e9, 1),
-                "balance_kernel_frac": round(alg["balance_kernel"] / (per["balance_kernel"] * 1e-3) / 1e9 / hbm, 4),
-                "note": "decompose is a dependent chain (see `chain`); its HBM fraction is "
-                        "reported for completeness only. balance is the HBM-bound kernel"}
+        traffic = json.load(open(tf)).get(f"decompose_kernel/n{n}_m{m}_B{B}")
     sm_hz = None
     try:
         sm_hz = torch.cuda.get_device_properties(0).clock_rate * 1e3
@@ -275,8 +264,31 @@ def bench_synth(args) -> dict:
     if not sm_hz:
         sm_hz = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
     peels = sum(n_raw) / len(n_raw)
-    roofline["decompose_cycles_per_peel"] = round(alone["decompose_kernel"] * 1e-3 * sm_hz / peels,
-                                                  1)
+    # The dominant kernel (decompose, 92 % of a batch) is a dependent
+    # shared-memory chain, not an HBM stream: its roofline is cycles per DFS
+    # step against the chain floor, filled in below from
+    # the oracle's DFS step count of the checked matrices.  Per-kernel device
+    # times come from the batch run alone (the in-flight overlap stretches
+    # every kernel's own event window).
+    bal_gbs = alg["balance_kernel"] / (alone["balance_kernel"] * 1e-3) / 1e9
+    dec_gbs = alg["decompose_kernel"] / (alone["decompose_kernel"] * 1e-3) / 1e9
+    roofline = {"bound": "latency", "kernel": "decompose_kernel",
+                "achieved": None, "peak": DFS_STEP_FLOOR_CYCLES,
+                "unit": "cycles per DFS step (whole kernel; lower is better, frac = peak/achieved)",
+                "frac": None, "traffic": traffic,
+                "algorithmic_bytes": alg["decompose_kernel"],
+                "kernel_ms_batch_alone": {k: round(v, 4) for k, v in alone.items()},
+                "kernel_ms_in_flight": {k: round(v, 4) for k, v in per.items()},
+                "decompose_cycles_per_peel": round(alone["decompose_kernel"] * 1e-3 * sm_hz / peels,
+                                                   1),
+                "hbm_view": {"bound": "hbm", "peak": hbm, "unit": "GB/s",
+                             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                             "decompose_kernel_gbs": round(dec_gbs, 1),
+                             "decompose_kernel_frac": round(dec_gbs / hbm, 5),
+                             "balance_kernel_gbs": round(bal_gbs, 1),
+                             "balance_kernel_frac": round(bal_gbs / hbm, 4),
+                             "note": "balance is the HBM-bound kernel; decompose's HBM fraction is "
+                                     "reported for completeness only"}}
 
     # ---- e2e: host (pinned) D -> device -> synth -> compact result -> host,
     # through the public host-buffer API (HostSynthPipeline: chunked, copies
@@ -340,6 +352,8 @@ def bench_synth(args) -> dict:
                   "by tests/golden/headline_digests.json)", "paths": ["device", "e2e"] if hs is not None
                   else ["device"], "result": "bit-exact"}
         cyc = alone["decompose_kernel"] * 1e-3 * sm_hz / steps_mean
+        roofline["achieved"] = round(cyc, 1)
+        roofline["frac"] = round(DFS_STEP_FLOOR_CYCLES / cyc, 4)
         roofline["chain"] = {
             "bound": "dependent shared-memory chain (Kuhn DFS)", "kernel": "decompose_kernel",
             "dfs_steps_per_matrix": round(steps_mean, 1),
