@@ -403,7 +403,10 @@ def single_matrix_latency(args) -> dict:
     stream = torch.cuda.current_stream()
     sh = ctypes.c_void_p(stream.cuda_stream)
     res = {}
-    for n in (16, 32, 64, 128):
+    # the paper's own synthesis times (C++ on a Xeon 8468):
+    # 4x8 25 us, 8x8 221 us, 12x8 805 us, 40x8 77 ms
+    paper = {4: 25.0, 8: 221.0, 12: 805.0, 40: 77000.0}
+    for n in (4, 8, 12, 16, 32, 40, 64, 128):
         G = n * args.m
         D = workloads.zipf_batch_device([0], G, args.skew, args.total, torch.device("cuda", 0))
         bufs = synth.SynthBuffers(1, n, args.m, D.device, compact=True)
@@ -420,7 +423,11 @@ def single_matrix_latency(args) -> dict:
                 times.append(a.elapsed_time(b))
         res[f"n{n}"] = {"us": round(statistics.median(times) * 1e3, 1),
                         "stages": int(bufs.n_raw.item())}
-    return {"what": "one matrix per call (B=1), device time, median", "unit": "us", **res}
+        if n in paper:
+            res[f"n{n}"]["paper_cpu_us"] = paper[n]
+    return {"what": "one matrix per call (B=1), device time, median; paper_cpu_us: the paper's "
+                    "published synthesis time for that server count (PAPER.md:550-551)",
+            "unit": "us", **res}
 
 
 def cpu_baseline_synth(args, D, budget_s: float = 12.0) -> tuple[dict, dict]:
