@@ -316,11 +316,10 @@ def run(args, workload: str) -> dict | None:
             "vs_baseline": None, "dtype": "u8",
             "data": f"synthetic (Zipf {args.a2a_skew} traffic, seed {args.seed}, random payload)",
             "config": {"workload": "config2_alltoallv", "virtual_servers": f"{n}x{m}",
-                       "total_bytes": total, "zipf_skew": args.a2a_skew,
-                       "bottleneck_gpu_bytes": direct_bn, "blocks_per_rank": args.blocks,
-                       "chunk_bytes": args.chunk,
-                       "l2": "payload per step %.0f MB; recv/staging are rewritten each step"
-                             % (total / 1e6)},
+                       "total_bytes": total, "zipf_skew": args.a2a_skew},
+            "bottleneck_gpu_bytes": direct_bn, "blocks_per_rank": args.blocks,
+            "chunk_bytes": args.chunk,
+            "l2": "payload per step %.0f MB; recv/staging are rewritten each step" % (total / 1e6),
             "algbw_gbps_per_gpu": round(algorithmic_bandwidth(total, G, step_ms * 1e-3) / 1e9, 3),
             "exec_kernel_ms": round(exec_ms, 4),
             "synth_and_plan_ms": round(step_ms - exec_ms, 4),
@@ -464,7 +463,7 @@ def reference_alltoallv(args, world: int) -> dict:
             "scaling": "strong", "vs_baseline": None, "dtype": "u8",
             "data": f"synthetic (Zipf {args.a2a_skew}, seed {args.seed})",
             "config": {"workload": "config2_alltoallv", "virtual_servers": f"{n}x{m}",
-                       "total_bytes": total},
+                       "total_bytes": total, "zipf_skew": args.a2a_skew},
             "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": 1, "kind": kind,
                              "sample": "tiersched.synthesize_fast + host memcpy of every "
                                        "segment (numpy, 1 thread), full 256 MiB per step"},
