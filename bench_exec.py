@@ -439,15 +439,26 @@ def reference_alltoallv(args, world: int) -> dict:
         def synth():
             oracle.synthesize_batch(D, n, m)
         kind = "port"
-    from oracle.alltoallv import direct_alltoallv
+    from concurrent.futures import ThreadPoolExecutor
 
     rng = np.random.default_rng(0)
     sends = [rng.integers(0, 256, int(D[g].sum()), dtype=np.uint8) for g in range(G)]
+    recvs = [np.empty(int(D[:, h].sum()), np.uint8) for h in range(G)]
+    send_off = np.concatenate([np.zeros((G, 1), np.int64), np.cumsum(D, axis=1)[:, :-1]], axis=1)
+    recv_off = np.concatenate([np.zeros((1, G), np.int64), np.cumsum(D, axis=0)[:-1, :]], axis=0)
+    segs = [(g, h) for g in range(G) for h in range(G) if D[g, h] > 0]
+    threads = os.cpu_count() or 1
+    pool = ThreadPoolExecutor(threads)
+
+    def copy_seg(gh):  # numpy releases the GIL while copying
+        g, h = gh
+        n_ = int(D[g, h])
+        recvs[h][recv_off[g, h]:recv_off[g, h] + n_] = sends[g][send_off[g, h]:send_off[g, h] + n_]
 
     def step():
         t = time.perf_counter()
         synth()
-        direct_alltoallv(sends, D)
+        list(pool.map(copy_seg, segs))  # the alltoallv the schedule describes, every host thread
         return time.perf_counter() - t
 
     for _ in range(args.warmup):
@@ -464,9 +475,10 @@ def reference_alltoallv(args, world: int) -> dict:
             "data": f"synthetic (Zipf {args.a2a_skew}, seed {args.seed})",
             "config": {"workload": "config2_alltoallv", "virtual_servers": f"{n}x{m}",
                        "total_bytes": total, "zipf_skew": args.a2a_skew},
-            "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": 1, "kind": kind,
-                             "sample": "tiersched.synthesize_fast + host memcpy of every "
-                                       "segment (numpy, 1 thread), full 256 MiB per step"},
+            "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": threads,
+                             "kind": kind,
+                             "sample": "tiersched.synthesize_fast + host memcpy of every segment "
+                                       f"(numpy, {threads} threads), full 256 MiB per step"},
             "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 
