@@ -61,7 +61,8 @@ class MoEDispatch:
         self.L = self.E // comm.world
         dev = comm.device
         lib = _lib.load()
-        self.topk = torch.empty(self.T * k, dtype=torch.int32, device=dev)
+        self._gate_topk = torch.empty(self.T * k, dtype=torch.int32, device=dev)
+        self.topk = self._gate_topk  # the ids of the last route (gate's or the router's)
         self.pos = torch.empty(self.T * k, dtype=torch.int32, device=dev)
         self.counts = torch.empty(self.E, dtype=torch.int64, device=dev)
         self.seg_rows = torch.empty(self.E, dtype=torch.int64, device=dev)
@@ -99,9 +100,7 @@ class MoEDispatch:
                 raise ValidationError("route needs the router's topk or a gate seed")
             if self.k != 2:
                 raise ValidationError("the synthetic gate is top-2; pass the router's topk")
-            if self.topk.numel() != self.T * self.k or self.topk.data_ptr() == 0:
-                self.topk = torch.empty(self.T * self.k, dtype=torch.int32,
-                                        device=self.comm.device)
+            self.topk = self._gate_topk  # never write into a router's tensor
             _lib.check_rc(lib.fast_moe_gate(self.T, ctypes.c_uint64(seed * 1000 + self.comm.rank),
                                             self.E, P(self.thr), P(self.thr2), P(self.topk), sh),
                           "fast_moe_gate")

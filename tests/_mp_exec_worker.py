@@ -76,6 +76,25 @@ def main() -> int:
             if not np.array_equal(gathered, D):
                 print(f"[rank {rank}] demand all-gather mismatch", flush=True)
                 ok = False
+        # graph replays with CHANGING counts in the same device tensor (the
+        # config-4 shifting hotspot): the device-side epoch, gather and
+        # synthesis must follow the new matrix on every replay
+        comm.set_fused(False)
+        row_t = torch.zeros(world, dtype=torch.int64, device="cuda")
+        for hot in range(3):
+            Dh = workloads.gen_hotspot(40 + hot, Topology(n, m), 20_000, hot=hot % world,
+                                       factor=8).sizes
+            sends_np = [payload(g, int(Dh[g].sum()) + 16) for g in range(world)]
+            sbuf = torch.zeros(cap, dtype=torch.uint8, device="cuda")
+            sbuf[: sends_np[rank].size].copy_(torch.from_numpy(sends_np[rank]))
+            row_t.copy_(torch.from_numpy(Dh[rank].copy()))
+            recv = comm.alltoallv(sbuf, row_t)
+            torch.cuda.synchronize()
+            comm.check()
+            want = direct_alltoallv(sends_np, Dh)[rank]
+            if not np.array_equal(recv[: len(want)].cpu().numpy(), want):
+                print(f"[rank {rank}] graph-replay mismatch n={n} m={m} hot={hot}", flush=True)
+                ok = False
         # all_to_all_fast vs NCCL all_to_all_single (rows of 4096 bf16)
         rng = np.random.default_rng(42)
         splits = rng.integers(0, 64, (world, world))
