@@ -225,6 +225,14 @@ int fast_plan_compile(const int64_t *D, const int64_t *send_self, int n, int m,
                       int64_t staging_capacity, int64_t chunk_bytes,
                       const fast_plan *plan, void *stream);
 
+/* fast_plan_compile with flags: FAST_PLAN_COPY_SELF also emits each rank's
+ * own segment (send_self bytes) as a local DIRECT op into its recv gap. */
+#define FAST_PLAN_COPY_SELF 1
+int fast_plan_compile_ex(const int64_t *D, const int64_t *send_self, int n, int m,
+                         const fast_sched_bufs *sched, int64_t recv_capacity,
+                         int64_t staging_capacity, int64_t chunk_bytes,
+                         const fast_plan *plan, int flags, void *stream);
+
 /* Same plan logic on HOST pointers -- validation/inspection only (CPU
  * tests); the executor never calls it.  `order/perm/sbytes` are one
  * matrix's packed stage arrays, K = n*n-2n+2. */
@@ -328,6 +336,13 @@ int fast_comm_set_fused(fast_comm *c, int enable);
 int fast_comm_set_send_rows(fast_comm *c, const void *rows_base,
                             const int32_t *row_src, int64_t row_bytes,
                             int64_t n_rows);
+/* fast_alltoallv also moves each rank's own segment (send_self bytes, kept
+ * in place in the send buffer) into the gap at its slot of the receive
+ * buffer, as one more local DIRECT op run by the exec CTAs alongside the
+ * remote sends (row-mapped if fast_comm_set_send_rows is active): the
+ * receive region is then the complete all_to_all_single output.  Off by
+ * default (the gap is the caller's). */
+int fast_comm_set_copy_self(fast_comm *c, int enable);
 /* Programmatic dependent launch on the fast_alltoallv chain (gather ->
  * synthesis -> plan -> exec: each kernel launches while its predecessor
  * runs and waits for its memory with griddepcontrol.wait); on by default. */

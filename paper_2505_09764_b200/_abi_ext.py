@@ -42,6 +42,7 @@ SIGNATURES: list[tuple[str, object, list]] = [
     ("fast_plan_workspace_bytes", ctypes.c_size_t, [I, I]),
     ("fast_plan_op_capacity", I64, [I, I]),
     ("fast_plan_compile", I, [V, V, I, I, P_SCHED, I64, I64, I64, P_PLAN, V]),
+    ("fast_plan_compile_ex", I, [V, V, I, I, P_SCHED, I64, I64, I64, P_PLAN, I, V]),
     ("fast_plan_compile_host", I, [V, V, I, I, I, V, V, V, I64, I64, I64, V, I64, V, V, V]),
     # communicator + P2P execution
     ("fast_comm_create", I, [I, I, I, I64, I64, ctypes.POINTER(V)]),
@@ -64,6 +65,7 @@ SIGNATURES: list[tuple[str, object, list]] = [
     ("fast_comm_set_send_rows", I, [V, V, V, I64, I64]),
     ("fast_comm_set_send_capacity", I, [V, I64]),
     ("fast_comm_set_pdl", I, [V, I]),
+    ("fast_comm_set_copy_self", I, [V, I]),
     ("fast_debug_copy", I, [V, V, I64, I, I64, I, V]),
     ("fast_debug_memcpy", I, [V, V, I64, V]),
     ("fast_comm_create_group", I, [I, I64, I64, ctypes.POINTER(V)]),

@@ -768,6 +768,7 @@ struct fast_comm {
   int row_l;
   int64_t send_cap;  // fast_comm_set_send_capacity (-1: unchecked)
   int no_pdl;        // 1: plain launches on the alltoallv chain
+  int copy_self;     // 1: the exec also copies each rank's own segment
 };
 
 static void set_rowmap(ExecArgs& a, const fast_comm* c) {
@@ -793,14 +794,25 @@ int64_t fast_plan_op_capacity(int n, int m) {
 static int plan_compile_launch(const int64_t* D, const int64_t* send_self, int n, int m,
                                const fast_sched_bufs* sched, int64_t recv_capacity,
                                int64_t staging_capacity, int64_t chunk_bytes,
-                               const fast_plan* plan, void* stream, bool pdl);
+                               const fast_plan* plan, void* stream, bool pdl,
+                               int copy_self = 0);
 
 int fast_plan_compile(const int64_t* D, const int64_t* send_self, int n, int m,
                       const fast_sched_bufs* sched, int64_t recv_capacity,
                       int64_t staging_capacity, int64_t chunk_bytes, const fast_plan* plan,
                       void* stream) {
   return plan_compile_launch(D, send_self, n, m, sched, recv_capacity, staging_capacity,
-                             chunk_bytes, plan, stream, false);
+                             chunk_bytes, plan, stream, false, 0);
+}
+
+int fast_plan_compile_ex(const int64_t* D, const int64_t* send_self, int n, int m,
+                         const fast_sched_bufs* sched, int64_t recv_capacity,
+                         int64_t staging_capacity, int64_t chunk_bytes, const fast_plan* plan,
+                         int flags, void* stream) {
+  if (flags & ~FAST_PLAN_COPY_SELF) return FAST_EVALIDATION;
+  return plan_compile_launch(D, send_self, n, m, sched, recv_capacity, staging_capacity,
+                             chunk_bytes, plan, stream, false,
+                             (flags & FAST_PLAN_COPY_SELF) ? 1 : 0);
 }
 
 }  // extern "C"
@@ -808,7 +820,7 @@ int fast_plan_compile(const int64_t* D, const int64_t* send_self, int n, int m,
 static int plan_compile_launch(const int64_t* D, const int64_t* send_self, int n, int m,
                                const fast_sched_bufs* sched, int64_t recv_capacity,
                                int64_t staging_capacity, int64_t chunk_bytes,
-                               const fast_plan* plan, void* stream, bool pdl) {
+                               const fast_plan* plan, void* stream, bool pdl, int copy_self) {
   if (!sched || !plan || n < 2 || m < 1 || m > FAST_MAX_GPUS_PER_SERVER) return FAST_EVALIDATION;
   fastplan::PlanIn in;
   in.n = n;
@@ -824,6 +836,7 @@ static int plan_compile_launch(const int64_t* D, const int64_t* send_self, int n
   in.staging_cap = staging_capacity;
   in.op_cap = plan->op_capacity;
   in.chunk = chunk_bytes & ~(int64_t)15;
+  in.copy_self = copy_self;
   fastplan::PlanOut out;
   out.ops = plan->ops;
   out.n_ops = plan->n_ops;
@@ -878,6 +891,7 @@ int fast_plan_compile_host(const int64_t* D, const int64_t* send_self, int n, in
   in.staging_cap = staging_capacity;
   in.op_cap = op_capacity;
   in.chunk = chunk_bytes & ~(int64_t)15;
+  in.copy_self = 0;
   int32_t status = 0;
   fastplan::PlanOut out;
   out.ops = ops;
@@ -1185,6 +1199,7 @@ static int launch_fused(fast_comm* c, const void* send, const int64_t* counts, i
   f.pin.staging_cap = c->staging_bytes;
   f.pin.op_cap = plan->op_capacity;
   f.pin.chunk = a.chunk;
+  f.pin.copy_self = c->copy_self;
   f.pout.ops = plan->ops;
   f.pout.n_ops = plan->n_ops;
   f.pout.staging_used = plan->staging_used;
@@ -1225,9 +1240,15 @@ int fast_alltoallv(fast_comm* c, const void* send, const int64_t* counts, int n,
   rc = fast_synth_batch_chain(D, 1, n, m, sched, (cudaStream_t)stream, pdl);
   if (rc != FAST_OK) return rc;
   rc = plan_compile_launch(D, D + (int64_t)c->world * c->world, n, m, sched, c->recv_bytes,
-                           c->staging_bytes, chunk_bytes, plan, stream, pdl);
+                           c->staging_bytes, chunk_bytes, plan, stream, pdl, c->copy_self);
   if (rc != FAST_OK) return rc;
   return exec_launch(c, plan, send, 0, blocks, chunk_bytes, timeline_ns, stream, 1, pdl);
+}
+
+int fast_comm_set_copy_self(fast_comm* c, int enable) {
+  if (!c) return FAST_EVALIDATION;
+  c->copy_self = enable ? 1 : 0;
+  return FAST_OK;
 }
 
 int fast_comm_set_pdl(fast_comm* c, int enable) {

@@ -79,6 +79,8 @@ struct PlanIn {
   int64_t recv_cap, staging_cap;
   int64_t op_cap;
   int64_t chunk;             // exec chunk size (flag granularity)
+  int copy_self;             // 1: also emit each rank's own segment as a local
+                             // DIRECT op (send_self bytes -> its recv gap)
 };
 
 struct PlanOut {
@@ -320,8 +322,9 @@ FAST_HD inline void plan_compile(const PlanIn& in, const PlanOut& out) {
     for (int p = 0; p < m; ++p)
       for (int q = 0; q < m; ++q) {
         const int g = i * m + p, h = i * m + q;
-        const int64_t len = in.D[(int64_t)g * G + h];
-        if (g != h && len > 0)
+        const int64_t len = g != h ? in.D[(int64_t)g * G + h]
+                                   : (in.copy_self && in.send_self ? in.send_self[g] : 0);
+        if (len > 0)
           sk.push(1, make_op(FAST_PH_DIRECT, FAST_STAGE_INTRA, g, FAST_BUF_SEND, w.send_off[(int64_t)g * G + h],
                              h, FAST_BUF_RECV, w.recv_off[(int64_t)g * G + h], len));
       }

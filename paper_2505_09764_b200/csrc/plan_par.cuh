@@ -369,6 +369,7 @@ __device__ __forceinline__ void plan_compile_par(const PlanIn& in, const PlanOut
       const int h = i * m + q;
       cnt += (h != r && in.D[(int64_t)r * G + h] > 0);
     }
+    if (in.copy_self && in.send_self && in.send_self[r] > 0) ++cnt;  // own segment, local
     w.direct_pre[r] = cnt;
   }
   for (int x = tid; x < S * n; x += nt) {  // bytes of (i -> j) in earlier stages
@@ -448,8 +449,9 @@ __device__ __forceinline__ void plan_compile_par(const PlanIn& in, const PlanOut
     int32_t at = s_nbal + w.direct_pre[g];
     for (int q = 0; q < m; ++q) {
       const int h = i * m + q;
-      const int64_t len = in.D[(int64_t)g * G + h];
-      if (h != g && len > 0)
+      const int64_t len = h != g ? in.D[(int64_t)g * G + h]
+                                 : (in.copy_self && in.send_self ? in.send_self[g] : 0);
+      if (len > 0)
         out.ops[at++] = make_op(FAST_PH_DIRECT, FAST_STAGE_INTRA, g, FAST_BUF_SEND, w.send_off[(int64_t)g * G + h],
                                 h, FAST_BUF_RECV, w.recv_off[(int64_t)g * G + h], len);
     }

@@ -194,6 +194,7 @@ class FastComm:
         self._graphs: dict = {}
         self._count_cache: dict = {}
         self._split_bad: torch.Tensor | None = None
+        self._copy_self = False  # state currently set in the C communicator
 
     def set_fused(self, enable: bool) -> None:
         """Single-launch path (gather + synthesis + plan inside the exec
@@ -230,10 +231,16 @@ class FastComm:
         ptr = lib.fast_comm_demand_ptr(self._ptr, 0) + 8 * self.world * self.world
         return bytes_view(ptr, self.world * 8, self.device).view(torch.int64)
 
+    def _set_copy_self(self, enable: bool) -> None:
+        if bool(enable) != self._copy_self:
+            _lib.check_rc(_lib.load().fast_comm_set_copy_self(self._ptr, 1 if enable else 0),
+                          "set_copy_self")
+            self._copy_self = bool(enable)
+
     def alltoallv(self, send: torch.Tensor, send_counts: torch.Tensor,
                   stream: torch.cuda.Stream | None = None, record_timeline: bool = False,
                   exec_events: tuple | None = None,
-                  send_rows: tuple | None = None) -> torch.Tensor:
+                  send_rows: tuple | None = None, copy_self: bool = False) -> torch.Tensor:
         """FAST alltoallv of `send` (uint8, device) split by send_counts
         (int64[world] device, bytes per destination in send order; the own
         entry is the self segment, which stays in place and is not moved).
@@ -245,6 +252,7 @@ class FastComm:
         its row r being row row_src[r] of `rows` (fused MoE pack -> send,
         fast_comm_set_send_rows); `send` is then only a placeholder."""
         lib = _lib.load()
+        self._set_copy_self(copy_self)
         if send_rows is None:
             return self._alltoallv(send, send_counts, stream, record_timeline, exec_events)
         rows, row_src, row_bytes = send_rows
@@ -278,7 +286,7 @@ class FastComm:
         tl = ctypes.c_void_p(self.timeline.data_ptr()) if record_timeline else None
         if exec_events is None:
             key = (send.data_ptr(), cap, row.data_ptr(), bool(record_timeline), self._fused,
-                   rows_key)
+                   rows_key, self._copy_self)
             g = self._graphs.get(key) if (self.use_graph and stream is None) else None
             if g is not None:  # one graph launch per call
                 g.replay()
@@ -303,11 +311,12 @@ class FastComm:
         _lib.check_rc(lib.fast_synth_batch(ctypes.c_void_p(dptr), 1, n, m,
                                            ctypes.byref(self.sched.struct), sh), "fast_synth_batch")
         sself = ctypes.c_void_p(dptr + 8 * self.world * self.world)
-        _lib.check_rc(lib.fast_plan_compile(ctypes.c_void_p(dptr), sself, n, m,
-                                            ctypes.byref(self.sched.struct), self.recv_bytes,
-                                            self.staging_bytes, self.chunk,
-                                            ctypes.byref(self.plan.struct), sh),
-                      "fast_plan_compile")
+        _lib.check_rc(lib.fast_plan_compile_ex(ctypes.c_void_p(dptr), sself, n, m,
+                                               ctypes.byref(self.sched.struct), self.recv_bytes,
+                                               self.staging_bytes, self.chunk,
+                                               ctypes.byref(self.plan.struct),
+                                               1 if self._copy_self else 0, sh),
+                      "fast_plan_compile_ex")
         exec_events[0].record(s)
         _lib.check_rc(lib.fast_exec(self._ptr, ctypes.byref(self.plan.struct),
                                     ctypes.c_void_p(send.data_ptr()), self.epoch, self.blocks,
@@ -426,13 +435,9 @@ def all_to_all_fast(output: torch.Tensor | None, input: torch.Tensor,
         raise ValidationError("output tensor smaller than sum(output_split_sizes)")
     inb = input.contiguous().view(torch.uint8).reshape(-1)
     counts = comm._counts_for(tuple(input_split_sizes), row_bytes)
-    recv = comm.alltoallv(inb, counts)
-    r = comm.rank
-    self_in = sum(input_split_sizes[:r]) * row_bytes
-    self_out = sum(output_split_sizes[:r]) * row_bytes
-    nself = input_split_sizes[r] * row_bytes
-    if nself:
-        recv[self_out:self_out + nself].copy_(inb[self_in:self_in + nself])
+    # the exec CTAs also move the own segment into its slot (a local op next
+    # to the remote sends), so the region is the complete output
+    recv = comm.alltoallv(inb, counts, copy_self=True)
     if check_splits:
         comm._check_output_splits(comm._counts_for(tuple(output_split_sizes), row_bytes, True))
     res = recv[:total_out].view(input.dtype).view(-1, *input.shape[1:])
@@ -526,7 +531,8 @@ class GroupComm:
                   stream: torch.cuda.Stream | None = None,
                   self_bytes: torch.Tensor | None = None,
                   send_rows: list | None = None,
-                  exec_events: tuple | None = None) -> list[torch.Tensor]:
+                  exec_events: tuple | None = None,
+                  copy_self: bool = False) -> list[torch.Tensor]:
         """D: [world, world] int64, zero diagonal.  self_bytes (optional,
         int64[world]): own segments kept in place in send_g and left as a
         gap in recv_g (all_to_all_single layout).  send_rows (optional, per
@@ -540,7 +546,8 @@ class GroupComm:
                     ctypes.c_void_p(row_src.data_ptr()), int(rb), row_src.numel()),
                     "fast_comm_set_send_rows")
             try:
-                return self.alltoallv(sends, D, stream, self_bytes, exec_events=exec_events)
+                return self.alltoallv(sends, D, stream, self_bytes, exec_events=exec_events,
+                                      copy_self=copy_self)
             finally:
                 for r in range(self.world):
                     lib.fast_comm_set_send_rows(self._ptrs[r], None, None, 0, 0)
@@ -555,10 +562,11 @@ class GroupComm:
         _lib.check_rc(lib.fast_synth_batch(dp, 1, n, m, ctypes.byref(self.sched.struct), sh),
                       "fast_synth_batch")
         sp_self = None if self._self is None else ctypes.c_void_p(self._self.data_ptr())
-        _lib.check_rc(lib.fast_plan_compile(dp, sp_self, n, m, ctypes.byref(self.sched.struct),
-                                            self.recv_bytes, self.staging_bytes, self.chunk,
-                                            ctypes.byref(self.plan.struct), sh),
-                      "fast_plan_compile")
+        _lib.check_rc(lib.fast_plan_compile_ex(dp, sp_self, n, m, ctypes.byref(self.sched.struct),
+                                               self.recv_bytes, self.staging_bytes, self.chunk,
+                                               ctypes.byref(self.plan.struct),
+                                               1 if copy_self else 0, sh),
+                      "fast_plan_compile_ex")
         sp = (ctypes.c_void_p * self.world)(*[s.data_ptr() for s in sends])
         if exec_events is not None:
             exec_events[0].record(stream or torch.cuda.current_stream())

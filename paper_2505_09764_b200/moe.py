@@ -47,7 +47,8 @@ class MoEDispatch:
     receives, per source, its experts' rows expert by expert."""
 
     def __init__(self, comm, tokens_per_gpu: int, row_bytes: int, k: int = 2,
-                 alpha: float = 0.8, fused_pack: bool = False, num_experts: int | None = None):
+                 alpha: float = 0.8, fused_pack: bool = False, num_experts: int | None = None,
+                 exec_self: bool = True):
         if row_bytes % 16:
             raise ValidationError("row_bytes must be a multiple of 16")
         if k not in (1, 2, 4, 8):
@@ -75,6 +76,9 @@ class MoEDispatch:
         self.row_src = torch.empty(self.T * k, dtype=torch.int32, device=dev)
         self.send = torch.empty(0 if fused_pack else self.T * k * row_bytes, dtype=torch.uint8,
                                 device=dev)
+        # FastComm: the exec kernel copies the own segment (FAST_PLAN_COPY_SELF);
+        # group-mode rank views keep the explicit unpack
+        self.exec_self = exec_self and hasattr(comm, "_set_copy_self")
         self.set_hot(0, alpha)
 
     def set_hot(self, hot: int, alpha: float = 0.8) -> None:
@@ -163,18 +167,23 @@ class MoEDispatch:
         source-major; per source this rank's experts in order; the row count
         is this rank's experts' counts summed over sources)."""
         self.route(seed, stream, topk)
+        # the own experts' rows: moved by the exec CTAs next to the remote
+        # sends (a local op of the plan) instead of a separate unpack after it
+        kw = {"copy_self": True} if self.exec_self else {}
         if self.fused_pack:
             self.rowmap(stream, tokens)
             self.comm.alltoallv(self._tokens, self.demand_row, stream=stream,
-                                send_rows=(self._tokens, self.row_src, self.row_bytes))
+                                send_rows=(self._tokens, self.row_src, self.row_bytes), **kw)
         else:
             self.pack(tokens, stream)
-            self.comm.alltoallv(self.send, self.demand_row, stream=stream)
+            self.comm.alltoallv(self.send, self.demand_row, stream=stream, **kw)
         # the demand matrix lands on `stream`: snapshot it there (not on the
         # current stream, which may run ahead of a side stream)
         s = stream or torch.cuda.current_stream()
         with torch.cuda.stream(s):
             self.remember_forward(self.comm.demand(), self.comm.self_sizes())
+        if self.exec_self:
+            return self.comm.recv
         return self.unpack(stream)
 
     def remember_forward(self, D: torch.Tensor, self_sizes: torch.Tensor) -> None:

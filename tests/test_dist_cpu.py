@@ -51,7 +51,8 @@ class _GlooComm:
         col = self.D[:, self.rank]
         self.split_errors += int((col != out_bytes).any())
 
-    def alltoallv(self, send: torch.Tensor, counts: torch.Tensor) -> torch.Tensor:
+    def alltoallv(self, send: torch.Tensor, counts: torch.Tensor,
+                  copy_self: bool = False) -> torch.Tensor:
         rows = [torch.zeros(self.world, dtype=torch.int64) for _ in range(self.world)]
         dist.all_gather(rows, counts.to(torch.int64))
         D = torch.stack(rows)
@@ -61,7 +62,8 @@ class _GlooComm:
         dist.all_to_all_single(recv[: int(sum(out_splits))], send[: int(counts.sum())], out_splits,
                                counts.tolist())
         lo = int(sum(out_splits[: self.rank]))
-        recv[lo:lo + out_splits[self.rank]] = 0  # the self slot is a gap
+        if not copy_self:
+            recv[lo:lo + out_splits[self.rank]] = 0  # the self slot is a gap
         return recv
 
 

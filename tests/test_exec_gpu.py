@@ -251,3 +251,27 @@ def test_group_exec_measured_timeline(n, m):
     ev_s = ev[0].elapsed_time(ev[1]) * 1e-3
     assert abs(max(totals) - ev_s) <= 0.05 * ev_s, (max(totals), ev_s)
     comm.close()
+
+
+@pytest.mark.parametrize("n,m", [(2, 2), (2, 4), (4, 2)])
+def test_group_exec_copy_self(n, m):
+    """FAST_PLAN_COPY_SELF: the exec CTAs also move each rank's own segment
+    (kept in place in its send buffer) into the gap at its receive slot, so
+    every receive buffer is the complete all_to_all_single output."""
+    G = n * m
+    D = workloads.zipf_sizes(7, G, 1.2, 2_000_003)
+    selfb = np.array([12_345 + 1_001 * g for g in range(G)], dtype=np.int64)
+    Dfull = D + np.diag(selfb)
+    cap = int(Dfull.sum(axis=0).max()) + 4096
+    comm = GroupComm(Topology(n, m), recv_bytes=cap, staging_bytes=2 * cap + (1 << 20), blocks=8,
+                     chunk_bytes=64 * 1024)
+    sends_np = [payload(g, int(Dfull[g].sum()) + 16) for g in range(G)]
+    recvs = comm.alltoallv([torch.from_numpy(x).cuda() for x in sends_np],
+                           torch.from_numpy(D).cuda(), self_bytes=torch.from_numpy(selfb).cuda(),
+                           copy_self=True)
+    torch.cuda.synchronize()
+    comm.check()
+    want = direct_alltoallv(sends_np, Dfull)
+    for h in range(G):
+        assert np.array_equal(recvs[h][: len(want[h])].cpu().numpy(), want[h]), h
+    comm.close()
