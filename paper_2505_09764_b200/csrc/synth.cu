@@ -150,7 +150,9 @@ __global__ void __launch_bounds__(kBalThreads)
       }
     }
     out.server[(int64_t)b * n * n + i * n + j] = s;
-    if (bad) {
+    // a tile at the 2^62 guard already puts the matrix total there: that is
+    // the model's validation error (model.py:26), not a balancing failure
+    if (bad || s >= kMaxSafeTotal) {
       raise_status(st, FAST_EVALIDATION);
     } else if (i != j) {
       const int T = n * (n - 1);
@@ -163,12 +165,6 @@ __global__ void __launch_bounds__(kBalThreads)
       if (nm < 0) {
         raise_status(st, FAST_EINVARIANT);
         nm = 0;
-      } else if (tp != s) {
-        // merge_peer (balance.py:129-136) / conservation (:157-163): the
-        // greedy ends with every row at its target, so max - min <= 1 and
-        // the rows keep the plain tile total; that total differs from the
-        // saturating one only past the 2^62 guard
-        raise_status(st, FAST_EINVARIANT);
       }
       out.move_count[(int64_t)b * T + tidx] = nm;
     }
@@ -177,6 +173,261 @@ __global__ void __launch_bounds__(kBalThreads)
   strip_rows<M>(sm, nullptr, Bb, m, G, Jc, false);
 }
 
+__host__ __device__ constexpr int ceil_log2(int x) { return x <= 1 ? 0 : 1 + ceil_log2((x + 1) / 2); }
+
+// ---------------------------------------------------------------------------
+// balance_reg_kernel<M> (even M <= 16, the default for those): the same per-tile
+// work as balance_kernel, with the strip staged through REGISTERS so each
+// thread has all M of its 16-byte row loads in flight at once (the staged
+// kernel issued one load per row and waited on it: 37 % of its stall samples
+// sat on that wait, profiles/r2_synth_ncu_full_summary.txt), and with the
+// per-tile prologue (row sums, the saturating server total, the validation
+// of balance_kernel's loop) done by all threads at load time instead of by
+// the one thread that balances the tile:
+//   * thread e owns column pair 2*(e % (M/2)) of tile e / (M/2) in every row;
+//   * the M/2 threads of a tile butterfly-reduce their row partial sums and
+//     the OR of their cells (a tile whose cells are all < 2^(62 - 2 log2 M)
+//     cannot reach the 2^62 guard, so its saturating total is the plain one;
+//     any other tile -- negative, huge -- takes balance_kernel's exact loop);
+// J = 128 / (M/2) tiles per CTA (32 at m = 8: one full warp balances them).
+// Load side of one strip (thread e < kBalThreads of the CTA): its M row pairs
+// are in x[]; stores them into the tile, reduces the tile's row sums and the
+// OR of its cells over the PPR threads of the tile (consecutive lanes).
+template <int M>
+__device__ __forceinline__ void bal_stage_in(const longlong2 (&x)[M], int64_t* __restrict__ sm,
+                                             int64_t* __restrict__ rsum,
+                                             uint64_t* __restrict__ tflag, const int e) {
+  constexpr int PPR = M / 2, TS = M * M + 1;
+  const int jj = e / PPR, c = 2 * (e % PPR);
+  int64_t* t = sm + jj * TS;
+  int64_t part[M];
+  uint64_t orv = 0;
+#pragma unroll
+  for (int r = 0; r < M; ++r) {
+    t[r * M + c] = x[r].x;
+    t[r * M + c + 1] = x[r].y;
+    part[r] = x[r].x + x[r].y;
+    orv |= (uint64_t)x[r].x | (uint64_t)x[r].y;
+  }
+  // a CTA edge tile (jj >= Jc) is skipped by all PPR lanes of its group together
+  const unsigned grp = (PPR >= 32) ? 0xffffffffu
+                                   : (((1u << PPR) - 1u) << ((e & 31) & ~(PPR - 1)));
+#pragma unroll
+  for (int off = 1; off < PPR; off <<= 1) {
+#pragma unroll
+    for (int r = 0; r < M; ++r) part[r] += __shfl_xor_sync(grp, part[r], off);
+    orv |= __shfl_xor_sync(grp, orv, off);
+  }
+  const int q = e % PPR;
+#pragma unroll
+  for (int r = 0; r < M; ++r)
+    if (r % PPR == q) rsum[jj * M + r] = part[r];
+  if (q == 0) tflag[jj] = orv;
+}
+
+// Tile (i, j) of matrix b, staged at t with its row sums / cell OR: server
+// total, validation, balance_senders, moves and mask (balance_kernel's
+// per-tile work with the prologue already reduced).
+template <int M>
+__device__ __forceinline__ void bal_tile_work(int64_t* __restrict__ t,
+                                              const int64_t* __restrict__ rsum_t,
+                                              const uint64_t orv, const int b, const int i,
+                                              const int j, const int n,
+                                              const fast_sched_bufs& out) {
+  constexpr int BITS = 62 - ceil_log2(M * M);  // M*M cells below 2^BITS sum below 2^62
+  int32_t* st = out.status + b;
+  int64_t rs[M];
+  bool bad = false;
+  int64_t s = 0, tp = 0;  // saturating / plain tile totals
+#pragma unroll
+  for (int p = 0; p < M; ++p) rs[p] = rsum_t[p];
+  if ((orv >> BITS) == 0) {
+#pragma unroll
+    for (int p = 0; p < M; ++p) tp += rs[p];
+    s = tp;
+    if (i == j)  // intra tile: the diagonal must be empty
+#pragma unroll
+      for (int p = 0; p < M; ++p) bad |= t[p * M + p] != 0;
+  } else {  // balance_kernel's exact loop (negative cells, the 2^62 guard)
+#pragma unroll
+    for (int p = 0; p < M; ++p) {
+      for (int q = 0; q < M; ++q) {
+        const int64_t v = t[p * M + q];
+        if (v < 0) { bad = true; continue; }
+        if (i == j && p == q && v != 0) bad = true;
+        s = sat_add(s, v);
+      }
+      tp += rs[p];
+    }
+  }
+  out.server[(int64_t)b * n * n + i * n + j] = s;
+  // a tile at the 2^62 guard already puts the matrix total there: that is
+  // the model's validation error (model.py:26), not a balancing failure
+  if (bad || s >= kMaxSafeTotal) {
+    raise_status(st, FAST_EVALIDATION);
+  } else if (i != j) {
+    const int T = n * (n - 1);
+    constexpr int slots = M > 1 ? M - 1 : 1;
+    const int tidx = i * (n - 1) + (j < i ? j : j - 1);
+    fast_move* mv = out.moves + ((int64_t)b * T + tidx) * slots;
+    uint64_t mk = 0;
+#ifdef FAST_BAL_NOCOMPUTE  // timing experiment only: the memory phases alone
+    int nm = 0;
+    (void)mv;
+#else
+    int nm = balance_tile<M>(t, M, mv, slots, rs, &mk);
+#endif
+    if (out.tile_mask) out.tile_mask[(int64_t)b * T + tidx] = mk;
+    if (nm < 0) {
+      raise_status(st, FAST_EINVARIANT);
+      nm = 0;
+    }
+    out.move_count[(int64_t)b * T + tidx] = nm;
+  }
+}
+
+#ifndef FAST_BAL_MINB
+#define FAST_BAL_MINB 8  // <= 64 registers: 8 CTAs of 128 threads per SM
+#endif
+template <int M>
+__global__ void __launch_bounds__(kBalThreads, M >= 16 ? 1 : FAST_BAL_MINB)
+    balance_reg_kernel(const int64_t* __restrict__ D, const int n,
+                       fast_sched_bufs out) {
+  static_assert(M % 2 == 0 && M <= 16, "even m <= 16");
+  constexpr int PPR = M / 2;                // 16-B pairs per tile row
+  constexpr int J = kBalThreads / PPR;      // tiles per CTA
+  constexpr int TS = M * M + 1;             // +1 word of padding per tile
+  extern __shared__ int64_t sm[];
+  int64_t* rsum = sm + J * TS;                                  // [J][M]
+  uint64_t* tflag = reinterpret_cast<uint64_t*>(rsum + J * M);  // [J]
+  pdl_trigger();
+  pdl_wait();
+  const int b = blockIdx.z, i = blockIdx.x, j0 = blockIdx.y * J;
+  const int Jc = min(J, n - j0);
+  const int64_t G = (int64_t)n * M;
+  const int64_t* Db = D + (int64_t)b * G * G + (int64_t)i * M * G + j0 * M;
+  int64_t* Bb = out.balanced + (int64_t)b * G * G + (int64_t)i * M * G + j0 * M;
+
+  const int e = threadIdx.x;
+  if (e / PPR < Jc) {
+    longlong2 x[M];
+#pragma unroll
+    for (int r = 0; r < M; ++r)
+      x[r] = __ldcs(reinterpret_cast<const longlong2*>(Db + r * G + 2 * e));
+    bal_stage_in<M>(x, sm, rsum, tflag, e);
+  }
+  __syncthreads();
+  if (threadIdx.x < Jc) {
+    const int jj = threadIdx.x;
+    bal_tile_work<M>(sm + jj * TS, rsum + jj * M, tflag[jj], b, i, j0 + jj, n, out);
+  }
+  __syncthreads();
+  strip_rows<M>(sm, nullptr, Bb, M, G, Jc, false);
+}
+
+#ifdef FAST_BAL_PIPE
+// ---------------------------------------------------------------------------
+// balance_pipe_kernel<M> (opt-in, -DFAST_BAL_PIPE; SLOWER, kept for the record): the
+// register-staged kernel as a persistent, software-pipelined loop over
+// strips.  kBalThreads load/store threads plus ceil(J/32) balancing warps
+// per CTA; while the balancing warps work on strip k, the load threads
+// already hold strip k+1's row loads in flight in registers, so the HBM
+// stream no longer stops for the sequential greedy (the register-staged
+// kernel spent 46 % of its stall samples at the barrier behind it and ran
+// its memory phases alone in 2.77 ms against 3.67 ms with the greedy).
+// Per strip: stage-in (the loaded registers -> tile, row sums) | barrier |
+// issue strip k+1's loads, balance strip k | barrier | store strip k.  A
+// load thread reads back in the store phase exactly the cells it staged in,
+// so the next stage-in needs no extra barrier.
+// Measured (n=128 x 8, B=1000, profiles/r2_balance_reg_ab.log): 4.98-5.70 ms
+// for 3-6 CTAs per SM against 3.66 ms for balance_reg_kernel: one strip in
+// flight per CTA and 4-6 CTAs per SM hold too few bytes in flight for HBM
+// (the memory phases alone: 2.95 ms, vs 2.77 ms in the register-staged kernel).
+template <int M>
+constexpr int bal_pipe_threads() {
+  return kBalThreads + ((kBalThreads / (M / 2) + 31) / 32) * 32;
+}
+#ifndef FAST_BAL_PIPE_MINB
+#define FAST_BAL_PIPE_MINB 5
+#endif
+template <int M>
+__global__ void __launch_bounds__(bal_pipe_threads<M>(), FAST_BAL_PIPE_MINB)
+    balance_pipe_kernel(const int64_t* __restrict__ D, const int n, const int nstrips,
+                        fast_sched_bufs out) {
+  static_assert(M % 2 == 0 && M <= 8, "even m <= 8");
+  constexpr int PPR = M / 2;
+  constexpr int J = kBalThreads / PPR;
+  constexpr int TS = M * M + 1;
+  extern __shared__ int64_t sm[];
+  int64_t* rsum = sm + J * TS;
+  uint64_t* tflag = reinterpret_cast<uint64_t*>(rsum + J * M);
+  pdl_trigger();
+  pdl_wait();
+  const int NJB = (n + J - 1) / J;
+  const int64_t G = (int64_t)n * M;
+  const int e = threadIdx.x;
+  const bool loader = e < kBalThreads;
+  // strip id -> (matrix b, server row i, first destination server j0)
+  auto decode = [&](int sid, int& b, int& i, int& j0) {
+    const int q = sid / NJB;
+    j0 = (sid - q * NJB) * J;
+    b = q / n;
+    i = q - b * n;
+  };
+  auto rows_at = [&](int b, int i, int j0) -> int64_t {
+    return (int64_t)b * G * G + (int64_t)i * M * G + j0 * M;
+  };
+  longlong2 x[M];
+  int sid = blockIdx.x;
+  if (loader && sid < nstrips) {
+    int b, i, j0;
+    decode(sid, b, i, j0);
+    if (e / PPR < min(J, n - j0)) {
+      const int64_t* Db = D + rows_at(b, i, j0);
+#pragma unroll
+      for (int r = 0; r < M; ++r)
+        x[r] = __ldcs(reinterpret_cast<const longlong2*>(Db + r * G + 2 * e));
+    }
+  }
+  for (; sid < nstrips; sid += gridDim.x) {
+    int b, i, j0;
+    decode(sid, b, i, j0);
+    const int Jc = min(J, n - j0);
+    const bool mine = loader && e / PPR < Jc;
+    if (mine) bal_stage_in<M>(x, sm, rsum, tflag, e);
+    __syncthreads();
+    if (loader) {
+      const int nsid = sid + gridDim.x;
+      if (nsid < nstrips) {
+        int nb, ni, nj0;
+        decode(nsid, nb, ni, nj0);
+        if (e / PPR < min(J, n - nj0)) {
+          const int64_t* Db = D + rows_at(nb, ni, nj0);
+#pragma unroll
+          for (int r = 0; r < M; ++r)
+            x[r] = __ldcs(reinterpret_cast<const longlong2*>(Db + r * G + 2 * e));
+        }
+      }
+    } else {
+      const int jj = e - kBalThreads;
+      if (jj < Jc) bal_tile_work<M>(sm + jj * TS, rsum + jj * M, tflag[jj], b, i, j0 + jj, n, out);
+    }
+    __syncthreads();
+    if (mine) {
+      const int jj = e / PPR, c = 2 * (e % PPR);
+      const int64_t* t = sm + jj * TS;
+      int64_t* Bb = out.balanced + rows_at(b, i, j0);
+#pragma unroll
+      for (int r = 0; r < M; ++r) {
+        longlong2 y;
+        y.x = t[r * M + c];
+        y.y = t[r * M + c + 1];
+        __stcs(reinterpret_cast<longlong2*>(Bb + r * G + 2 * e), y);
+      }
+    }
+  }
+}
+#endif  // FAST_BAL_PIPE
 
 #ifdef FAST_BAL_TMA
 // ---------------------------------------------------------------------------
@@ -291,7 +542,9 @@ __global__ void __launch_bounds__(kTmaTiles)
       tp += r;
     }
     out.server[(int64_t)b * n * n + i * n + j] = s;
-    if (bad) {
+    // a tile at the 2^62 guard already puts the matrix total there: that is
+    // the model's validation error (model.py:26), not a balancing failure
+    if (bad || s >= kMaxSafeTotal) {
       raise_status(st, FAST_EVALIDATION);
     } else if (i != j) {
       const int tidx = i * (n - 1) + (j < i ? j : j - 1);
@@ -302,8 +555,6 @@ __global__ void __launch_bounds__(kTmaTiles)
       if (nm < 0) {
         raise_status(st, FAST_EINVARIANT);
         nm = 0;
-      } else if (tp != s) {
-        raise_status(st, FAST_EINVARIANT);
       }
       out.move_count[(int64_t)b * T + tidx] = nm;
     }
@@ -636,6 +887,62 @@ int launch_balance(const int64_t* D, int B, int n, int m,
   // 262M TMA operations per batch, and the TMA issue rate, not HBM, bounds it.
   if (m == 8 && n >= kTmaTiles && (int64_t)B * n >= 2048)
     return launch_balance_tma<8>(D, B, n, out, s);
+#endif
+#if defined(FAST_BAL_PIPE) && !defined(FAST_BAL_STAGED)
+  // opt-in: the persistent pipelined kernel (measured slower, see above)
+  if (m == 2 || m == 4 || m == 8) {
+    const int J = kBalThreads / (m / 2);
+    const size_t smem = (size_t)J * ((m * m + 1) * 8 + m * 8 + 8);
+    const int64_t strips64 = (int64_t)B * n * ((n + J - 1) / J);
+    if (strips64 <= INT32_MAX) {
+      const int strips = (int)strips64;
+      static int per_sm[9] = {0}, sms = 0;
+      cudaError_t e = cudaSuccess;
+      if (!sms) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+          return FAST_ECUDA;
+      }
+#define FAST_BAL_PIPE_CASE(MV)                                                              \
+  case MV: {                                                                           \
+    if (!per_sm[MV] && cudaOccupancyMaxActiveBlocksPerMultiprocessor(                  \
+                           &per_sm[MV], balance_pipe_kernel<MV>,                       \
+                           bal_pipe_threads<MV>(), smem) != cudaSuccess)                \
+      return FAST_ECUDA;                                                               \
+    const int g = min(strips, sms * max(per_sm[MV], 1));                               \
+    e = launch_k(balance_pipe_kernel<MV>, dim3(g), dim3(bal_pipe_threads<MV>()), smem, \
+                 s, pdl, D, n, strips, *out);                                          \
+    break;                                                                             \
+  }
+      switch (m) {
+        FAST_BAL_PIPE_CASE(2)
+        FAST_BAL_PIPE_CASE(4)
+        FAST_BAL_PIPE_CASE(8)
+      }
+#undef FAST_BAL_PIPE_CASE
+      if (e != cudaSuccess) return FAST_ECUDA;
+      return check(cudaGetLastError());
+    }
+  }
+#endif
+#ifndef FAST_BAL_STAGED
+  // even m <= 16: the register-staged kernel (all row loads of a thread in
+  // flight, tile prologue at load time); -DFAST_BAL_STAGED for the A/B
+  if (m == 2 || m == 4 || m == 8 || m == 16) {
+    const int J = kBalThreads / (m / 2);
+    const size_t smem = (size_t)J * ((m * m + 1) * 8 + m * 8 + 8);
+    const dim3 grid(n, (n + J - 1) / J, B);
+    cudaError_t e = cudaSuccess;
+    switch (m) {
+      case 2: e = launch_k(balance_reg_kernel<2>, grid, dim3(kBalThreads), smem, s, pdl, D, n, *out); break;
+      case 4: e = launch_k(balance_reg_kernel<4>, grid, dim3(kBalThreads), smem, s, pdl, D, n, *out); break;
+      case 8: e = launch_k(balance_reg_kernel<8>, grid, dim3(kBalThreads), smem, s, pdl, D, n, *out); break;
+      default: e = launch_k(balance_reg_kernel<16>, grid, dim3(kBalThreads), smem, s, pdl, D, n, *out);
+    }
+    if (e != cudaSuccess) return FAST_ECUDA;
+    return check(cudaGetLastError());
+  }
 #endif
   const size_t tile_bytes = (size_t)(m * m + 1) * 8;
   // ~32 KiB strips: several CTAs per SM overlap the per-tile sequential

@@ -35,7 +35,7 @@ __host__ __device__ __forceinline__ int stage_cap(int n) {
 // balance_senders (balance.py:77-126) on one m x m tile in shared memory.
 // Returns the number of moves, or -1 if an invariant breaks.
 template <int M>
-__device__ int balance_tile(int64_t* __restrict__ t, const int m_rt,
+__device__ __forceinline__ int balance_tile(int64_t* __restrict__ t, const int m_rt,
                             fast_move* __restrict__ out, const int slots,
                             const int64_t* rowsum = nullptr,
                             uint64_t* changed = nullptr) {

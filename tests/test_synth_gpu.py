@@ -23,13 +23,14 @@ from paper_2505_09764_b200 import synth
 pytestmark = pytest.mark.gpu
 
 
-def _packed_equal(gpu_bufs: synth.SynthBuffers, ref: dict, B: int, n: int, m: int):
+def _packed_equal(gpu_bufs: synth.SynthBuffers, ref: dict, B: int, n: int, m: int,
+                  only=None):
     """Compare device output with the oracle's, matrix by matrix."""
     h = {k: getattr(gpu_bufs, k).cpu().numpy() for k in (
         "balanced", "server", "move_count", "common_sum", "aux", "n_raw", "n_stages",
         "status", "stage_weight", "stage_perm", "stage_bytes", "stage_order")}
     moves = gpu_bufs.moves.cpu().numpy().view(oracle.MOVE_DTYPE).reshape(ref["moves"].shape)
-    for b in range(B):
+    for b in (range(B) if only is None else only):
         assert h["status"][b] == ref["status"][b] == 0, b
         for k in ("balanced", "server", "move_count", "aux"):
             assert np.array_equal(h[k][b], ref[k][b]), (k, b)
@@ -126,6 +127,32 @@ def test_gpu_validation_errors_and_status():
     assert bufs.status.cpu().tolist() == [0, 2, 2, 2]
     with pytest.raises(ValidationError):
         synth.decompose(np.array([[1, 2], [0, 1]], np.int64))
+
+
+@pytest.mark.parametrize("m", [4, 8, 16])
+def test_gpu_balance_wide_cells_and_invalid_tiles(m):
+    """The register-staged balance kernel's exact fallback: tiles with cells
+    at or above 2^(62 - ceil(log2 m^2)) (valid, and past the 2^62 guard), negative
+    cells and non-zero diagonals, next to ordinary tiles of the same CTA."""
+    n, B = 3, 12
+    G = n * m
+    rng = np.random.default_rng(m)
+    D = rng.integers(0, 1 << 30, size=(B, G, G), dtype=np.int64)
+    D[:, np.arange(G), np.arange(G)] = 0
+    big = 1 << (62 - int(np.ceil(np.log2(m * m))))  # first width past the fast path
+    D[1, 0, m + 1] = big                     # wide cell, total stays below 2^62
+    D[2, 1, 2 * m] = (1 << 61) - 5           # wide cells over 2^62 in one tile
+    D[2, 2, 2 * m + 1] = (1 << 61) - 3
+    D[3, 0, 1] = 7                           # diagonal tile entry (0, 1) is off-diagonal: valid
+    D[4, m + 2, m + 2] = 9                   # diagonal cell
+    D[5, 2, m + 3] = -1                      # negative
+    D[6, 2 * m + 1, 1] = big - 1
+    ref = oracle.synthesize_batch(D, n, m)
+    bufs = synth.synthesize_packed(torch.from_numpy(D).cuda(), n, m)
+    st = bufs.status.cpu().tolist()
+    assert st == ref["status"].tolist()
+    _packed_equal(bufs, ref, B, n, m, only=[b for b in range(B) if st[b] == 0])
+    assert st[2] == 2 and st[4] == 2 and st[5] == 2 and st[1] == 0 and st[6] == 0
 
 
 def test_gpu_deterministic_across_runs():
