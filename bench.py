@@ -303,34 +303,58 @@ def bench_synth(args) -> dict:
         Dh.copy_(D)
         del bufs, sets
         torch.cuda.empty_cache()
-        pipe = synth.HostSynthPipeline(B, n, m, chunk=args.e2e_chunk, depth=2)
-        outs = [synth.HostSchedules(B, n, m), synth.HostSchedules(B, n, m)]
-        pipe.run([Dh, Dh], outs)  # warm-up (sizes the host value buffers)
+        depth = max(1, args.e2e_depth)
+        pipe = synth.HostSynthPipeline(B, n, m, chunk=args.e2e_chunk, depth=depth)
+        nout = max(2, depth)
+        outs = [synth.HostSchedules(B, n, m) for _ in range(nout)]
+        pipe.run([Dh] * nout, outs)  # sizes the host value buffers
         K = max(4, args.steps)
+        Wb = max(args.warmup, nout)
+        # one continuous stream of Wb + K batches (at most `depth` in flight);
+        # the timed window runs from the completion of the last warm-up batch
+        # to the completion of the K-th timed batch, so it holds K batches'
+        # worth of H2D, kernels and D2H in steady state (the pipeline's fill
+        # is the warm-up's, reported apart as fill_ms)
         torch.cuda.synchronize()
-        t0h = time.perf_counter()
-        done = pipe.run([Dh] * K, [outs[k % 2] for k in range(K)])
-        ems = (time.perf_counter() - t0h) * 1e3 / K
-        hs = done[-1]
-        if any(int(h.status.abs().max()) != 0 for h in done):
-            raise RuntimeError("e2e synthesis reported failures")
+        pending, comp = [], []
+        t_sub0 = time.perf_counter()
+
+        def complete():
+            h = pipe.result(pending.pop(0))
+            comp.append(time.perf_counter())
+            if int(h.status.abs().max()) != 0:
+                raise RuntimeError("e2e synthesis reported failures")
+            return h
+
+        for t in range(Wb + K):
+            pending.append(pipe.submit(Dh, outs[t % nout]))
+            if len(pending) >= depth:
+                hs = complete()
+        while pending:
+            hs = complete()
+        ems = (comp[Wb + K - 1] - comp[Wb - 1]) * 1e3 / K
+        fill_ms = (comp[0] - t_sub0) * 1e3
         torch.cuda.synchronize()
         t1h = time.perf_counter()
         pipe.result(pipe.submit(Dh, outs[0]))
         sync_ms = (time.perf_counter() - t1h) * 1e3
+        hs = outs[0]
         del pipe
         e2e = {"value": round(B / (ems * 1e-3), 3), "unit": "matrices/s",
                "h2d_bytes_per_step": int(Dh.numel() * 8), "d2h_bytes_per_step": int(hs.nbytes()),
-               "ms_per_step": round(ems, 3), "steps": K,
+               "ms_per_step": round(ems, 3), "steps": K, "warmup_batches": Wb,
+               "batches_in_flight": depth, "fill_ms": round(fill_ms, 3),
                "sync_ms_per_batch": round(sync_ms, 3),
                "sync_value": round(B / (sync_ms * 1e-3), 3),
                "d2h_full_device_layout_bytes": d2h_device_layout,
                "path": f"HostSynthPipeline (public host-buffer API: C-ABI fast_synth_batch + "
                        f"fast_compact_batch per {args.e2e_chunk}-matrix chunk), pinned host D in, "
                        "compact schedule out (HostSchedules: moves, stages, aux run-out table, "
-                       "changed cells of the balanced tiles); a stream of K batches, batch k+1 "
-                       "enqueued before batch k completes, wall clock incl. the final host sync; "
-                       "sync_*: one synchronous call"}
+                       "changed cells of the balanced tiles); one continuous stream of "
+                       "warm-up + K batches, timed (wall clock, host sync on each result) from "
+                       "the last warm-up batch's completion to the K-th timed batch's: K "
+                       "batches' H2D + D2H in steady state; fill_ms: first batch's latency in "
+                       "the stream; sync_*: one synchronous call"}
 
     cpu, parity = None, None
     if not args.no_cpu_baseline:
@@ -576,6 +600,7 @@ def main() -> None:
                     help="config 5: batches in flight (rotating buffer sets / streams)")
     ap.add_argument("--experts", type=int, default=8)
     ap.add_argument("--e2e-chunk", type=int, default=125)
+    ap.add_argument("--e2e-depth", type=int, default=2, help="HostSynthPipeline buffer sets")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 

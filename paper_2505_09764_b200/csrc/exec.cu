@@ -515,7 +515,7 @@ __device__ bool fused_prologue(const FusedArgs& f, uint8_t* const* peers, int ra
         sum = sat_add(sum, v);
       }
     f.sched.server[i * n + j] = sum;
-    if (bad) {
+    if (bad || sum >= kMaxSafeTotal) {  // past the 2^62 guard: model.py:26
       raise_status(f.sched.status, FAST_EVALIDATION);
     } else if (i != j) {
       const int tidx = i * (n - 1) + (j < i ? j : j - 1);

@@ -434,17 +434,16 @@ class HostSynthPipeline:
         return out
 
     def run(self, batches, outs) -> list[HostSchedules]:
-        """Stream batches through the pipeline: batch t+1 is enqueued before
-        batch t is completed.  outs[t] receives batch t (reuse two objects
-        alternately for a steady stream)."""
-        pending, done = None, []
+        """Stream batches through the pipeline: up to `depth` batches are
+        enqueued before the oldest is completed.  outs[t] receives batch t
+        (rotate `depth` objects for a steady stream)."""
+        pending, done = [], []
         for D_host, out in zip(batches, outs):
-            t = self.submit(D_host, out)
-            if pending is not None:
-                done.append(self.result(pending))
-            pending = t
-        if pending is not None:
-            done.append(self.result(pending))
+            pending.append(self.submit(D_host, out))
+            if len(pending) >= len(self.sets):
+                done.append(self.result(pending.pop(0)))
+        while pending:
+            done.append(self.result(pending.pop(0)))
         return done
 
 

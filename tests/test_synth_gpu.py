@@ -190,6 +190,40 @@ def test_gpu_compact_layout_matches_golden(golden_schedules):
     assert total > 300
 
 
+@pytest.mark.parametrize("depth", [1, 2, 3])
+def test_gpu_host_pipeline_stream_matches_oracle(depth):
+    """HostSynthPipeline.run: a stream of distinct batches with `depth`
+    buffer sets in rotation (several batches in flight) -- every batch's
+    compact host result equals the oracle's."""
+    n, m, B, K = 12, 4, 9, 5
+    G = n * m
+    Ds = []
+    for t in range(K):
+        rng = np.random.default_rng(100 + t)
+        D = rng.integers(0, 1 << 32, size=(B, G, G), dtype=np.int64)
+        D[rng.random(D.shape) < 0.2] = 0
+        D[:, np.arange(G), np.arange(G)] = 0
+        Ds.append(D)
+    pipe = synth.HostSynthPipeline(B, n, m, chunk=4, depth=depth)
+    outs = [synth.HostSchedules(B, n, m) for _ in range(max(2, depth))]
+    done = pipe.run([torch.from_numpy(D).pin_memory() for D in Ds],
+                    [outs[t % len(outs)] for t in range(K)])
+    assert len(done) == K
+    # each result is read before its HostSchedules object is reused: check the
+    # last len(outs) batches (the earlier ones were overwritten by design)
+    for t in range(K - len(outs), K):
+        hs, D = done[t], Ds[t]
+        ref = oracle.synthesize_batch(D, n, m)
+        for b in range(B):
+            p = hs.packed(b, D[b])
+            want = oracle.packed_fields(ref, b, n, m)
+            for key in ("balanced", "move_count", "stage_weight", "stage_perm", "stage_bytes",
+                        "stage_order"):
+                assert np.array_equal(getattr(p, key), want[key]), (key, t, b)
+            used = np.arange(want["moves"].shape[1])[None, :] < want["move_count"][:, None]
+            assert np.array_equal(p.moves[used], want["moves"][used]), (t, b)
+
+
 @pytest.mark.parametrize("n,m", [(16, 8), (8, 8), (5, 3), (3, 1)])
 def test_gpu_compact_layout_matches_oracle(n, m):
     rng = np.random.default_rng(7 * n + m)
