@@ -3,13 +3,16 @@
 // Three stream-ordered kernels replace tiersched.synthesize_fast
 // (pipeline.py:52-59) for a whole batch of demand matrices:
 //
-//   balance_kernel   build_balance_plan + reduce_to_server_level
+//   balance_reg_kernel / balance_kernel
+//                    build_balance_plan + reduce_to_server_level
 //                    (balance.py:77-174, model.py:169-178).  One CTA per
 //                    (server row i, block of J destination servers); the
 //                    m rows x J*m columns strip is staged into shared memory
-//                    with coalesced loads, one thread balances one m x m
-//                    cross tile in place, the strip is written back
-//                    coalesced.  HBM-bound: 8*G^2 B read + 8*G^2 B written.
+//                    with coalesced loads (even m <= 16: every row load of a
+//                    thread in flight at once, tile row sums reduced by the
+//                    loading threads), one thread balances one m x m cross
+//                    tile in place, the strip is written back coalesced.
+//                    HBM-bound: 8*G^2 B read + 8*G^2 B written.
 //   decompose_kernel embed_doubly_stochastic + decompose + strip_auxiliary
 //                    (birkhoff.py:75-252).  One warp per matrix.  Support of
 //                    the work matrix is a bitset in shared memory; the Kuhn
