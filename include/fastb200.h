@@ -97,7 +97,8 @@ size_t fast_synth_workspace_bytes(int B, int n);
  * (balance.py:139-174), reduce_to_server_level (model.py:169-178),
  * decompose_server_matrix (birkhoff.py:269-280), strip_auxiliary
  * (birkhoff.py:225-252), sort_stages_ascending (birkhoff.py:255-266).
- * D: device int64 [B][G][G]. */
+ * D: device int64 [B][G][G]; for even m, D and out->balanced must be
+ * 16-byte aligned (cudaMalloc'd / torch storage is), else FAST_EVALIDATION. */
 int fast_synth_batch(const int64_t *D, int B, int n, int m,
                      const fast_sched_bufs *out, void *stream);
 

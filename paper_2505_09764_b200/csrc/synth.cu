@@ -883,6 +883,9 @@ int launch_balance_tma(const int64_t* D, int B, int n, const fast_sched_bufs* ou
 
 int launch_balance(const int64_t* D, int B, int n, int m,
                    const fast_sched_bufs* out, cudaStream_t s, bool pdl = false) {
+  // even m moves 16-byte pairs of D / balanced: refuse misaligned views
+  // loudly instead of faulting on the device
+  if (m % 2 == 0 && (((uintptr_t)D | (uintptr_t)out->balanced) & 15)) return FAST_EVALIDATION;
 #ifdef FAST_BAL_TMA
   // opt-in: the TMA-fed per-thread pipeline.  Measured 2.3x SLOWER than the
   // staged kernel below (13.0 vs 5.6 ms at n=128 x 8, B=1000;

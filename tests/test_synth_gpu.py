@@ -155,6 +155,21 @@ def test_gpu_balance_wide_cells_and_invalid_tiles(m):
     assert st[2] == 2 and st[4] == 2 and st[5] == 2 and st[1] == 0 and st[6] == 0
 
 
+def test_gpu_misaligned_demand_view_is_rejected():
+    """Even m moves 16-byte pairs: an 8-byte-offset view of D is refused with
+    ValidationError (never a device fault), and the aligned copy works."""
+    n, m, B = 3, 2, 2
+    G = n * m
+    base = torch.zeros(B * G * G + 1, dtype=torch.int64, device="cuda")
+    D = base[1:].view(B, G, G)
+    D[:, 0, 3] = 5
+    assert D.data_ptr() % 16 == 8
+    with pytest.raises(ValidationError):
+        synth.synthesize_packed(D, n, m)
+    bufs = synth.synthesize_packed(D.clone(), n, m)
+    assert bufs.status.cpu().tolist() == [0, 0]
+
+
 def test_gpu_deterministic_across_runs():
     n, m, B = 32, 8, 8
     D = np.stack([workloads.zipf_sizes(b, n * m, 1.2, 2**34) for b in range(B)])
