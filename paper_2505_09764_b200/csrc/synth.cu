@@ -1069,7 +1069,7 @@ int fast_debug_dec_prof(unsigned long long* out8, int reset) {
 int fast_version(void) { return 200; }
 
 size_t fast_synth_workspace_bytes(int B, int n) {
-  if (B <= 0 || n < 2 || n > FAST_MAX_SERVERS) return 0;
+  if (B <= 0 || n < 1 || n > FAST_MAX_SERVERS) return 0;  // n = 1: decompose only
   return (size_t)B * dec_ws_bytes_per_matrix(n);
 }
 
@@ -1102,7 +1102,9 @@ int fast_balance_batch(const int64_t* D, int B, int n, int m,
 
 int fast_decompose_batch(const int64_t* S, int B, int n, int mode,
                          const fast_sched_bufs* out, void* stream) {
-  if (bad_shape(B, n, 1) || !out) return FAST_EVALIDATION;
+  // a 1 x 1 matrix is a valid decompose input (birkhoff.py:140); the
+  // synthesis entry points keep the topology's n >= 2 (model.py:55)
+  if (B < 0 || n < 1 || n > FAST_MAX_SERVERS || !out) return FAST_EVALIDATION;
   if (mode != FAST_DEC_SERVER && mode != FAST_DEC_DOUBLY_STOCHASTIC)
     return FAST_EVALIDATION;
   if (B == 0) return FAST_OK;

@@ -239,6 +239,13 @@ def decompose(embedded: np.ndarray) -> list[PermutationStage]:
         raise ValidationError("decompose expects a square matrix")
     if not np.issubdtype(e.dtype, np.integer):
         raise ValidationError("decompose expects an integer matrix")
+    # the reference's remaining checks, with its messages (birkhoff.py:155-163);
+    # the kernel checks the same on the device (status 2)
+    if np.any(e < 0):
+        raise ValidationError("decompose expects non-negative entries")
+    rows, cols = e.sum(axis=1), e.sum(axis=0)
+    if e.size and not (np.all(rows == rows[0]) and np.all(cols == rows[0])):
+        raise ValidationError("decompose expects equal row and column sums")
     p = _decompose_packed(e.astype(np.int64), _lib.FAST_DEC_DOUBLY_STOCHASTIC)
     _raise_status(p.status, "decompose")
     return list(p.raw_stages())
