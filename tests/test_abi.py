@@ -42,7 +42,8 @@ def test_library_exports_every_declared_symbol():
 def test_workspace_sizing_is_host_only():
     lib = _lib.load()
     assert lib.fast_synth_workspace_bytes(0, 8) == 0
-    assert lib.fast_synth_workspace_bytes(10, 1) == 0
+    assert lib.fast_synth_workspace_bytes(10, 0) == 0
+    assert lib.fast_synth_workspace_bytes(10, 1) == 10 * 256  # 1 x 1 decompose inputs
     assert lib.fast_synth_workspace_bytes(10, 129) == 0
     assert lib.fast_synth_workspace_bytes(1000, 128) > 1000 * 2 * 128 * 128 * 8
 
