@@ -255,6 +255,12 @@ def decompose(embedded: np.ndarray) -> list[PermutationStage]:
 _COMPACT_FIELDS = ("server", "move_count", "moves", "common_sum", "aux", "n_raw",
                    "stage_weight", "stage_perm", "n_stages", "stage_order", "status", "strip",
                    "tile_mask")
+# m > 8 (no 64-bit changed-cell mask per tile): the balanced matrix itself
+_WIDE_FIELDS = _COMPACT_FIELDS[:-1] + ("balanced",)
+
+
+def _host_fields(m: int) -> tuple:
+    return _COMPACT_FIELDS if m <= 8 else _WIDE_FIELDS
 
 
 class HostSchedules:
@@ -267,11 +273,10 @@ class HostSchedules:
     tiles as changed-cell masks + values (`tile_mask`, `vals`; replaces the
     G x G balanced matrix, which is D outside those cells).  ``packed(b, D)``
     decodes one matrix into the full PackedSchedule (and thus the reference
-    dataclasses / canonical JSON)."""
+    dataclasses / canonical JSON).  For m > 8 the G x G balanced matrix
+    itself is copied instead of the masks and values."""
 
     def __init__(self, B: int, n: int, m: int, vals_capacity: int | None = None):
-        if m > 8:
-            raise ValidationError("the compact host layout needs m <= 8")
         G, T, S, K = n * m, n * (n - 1), max(m - 1, 1), stage_cap(n)
         shapes = {"server": ((B, n, n), torch.int64),
                   "move_count": ((B, T), torch.int32), "moves": ((B, T, S, 2), torch.int64),
@@ -280,7 +285,9 @@ class HostSchedules:
                   "stage_perm": ((B, K, n), torch.uint8), "n_stages": ((B,), torch.int32),
                   "stage_order": ((B, K), torch.int32), "status": ((B,), torch.int32),
                   "strip": ((B, 2 * n + 2, 2), torch.int64),
-                  "tile_mask": ((B, max(T, 1)), torch.int64)}
+                  "tile_mask": ((B, max(T, 1)), torch.int64), "balanced": ((B, G, G), torch.int64)}
+        shapes = {k: shapes[k] for k in _host_fields(m)}
+        self.fields = _host_fields(m)
         self.B, self.n, self.m = B, n, m
         for k, (shape, dt) in shapes.items():
             setattr(self, k, torch.empty(shape, dtype=dt, pin_memory=True))
@@ -291,7 +298,7 @@ class HostSchedules:
 
     def fixed_nbytes(self) -> int:
         return sum(getattr(self, k).numel() * getattr(self, k).element_size()
-                   for k in _COMPACT_FIELDS)
+                   for k in self.fields)
 
     def nbytes(self) -> int:
         """Bytes copied device -> host by the last synthesize_host_batch."""
@@ -306,9 +313,12 @@ class HostSchedules:
         strip = self.strip[b].numpy().view(STRIP_DTYPE).reshape(-1)
         v0, v1 = int(self.val_base[b]), int(self.val_base[b + 1])
         st = int(self.status[b])
-        bal = (balanced_from_compact(D, self.tile_mask[b].numpy().view(np.uint64),
-                                     self.vals[v0:v1].numpy(), n, m)
-               if st == 0 else np.array(D, dtype=np.int64))
+        if m > 8:
+            bal = self.balanced[b].numpy() if st == 0 else np.array(D, dtype=np.int64)
+        else:
+            bal = (balanced_from_compact(D, self.tile_mask[b].numpy().view(np.uint64),
+                                         self.vals[v0:v1].numpy(), n, m)
+                   if st == 0 else np.array(D, dtype=np.int64))
         moves = self.moves[b].numpy().view(MOVE_DTYPE).reshape(self.moves.shape[1:3])
         return PackedSchedule(
             n=n, m=m, status=st, balanced=bal, server=self.server[b].numpy(),
@@ -349,8 +359,8 @@ class HostSynthPipeline:
                 bufs=[SynthBuffers(nb, n, m, dev, compact=True) for nb in sizes],
                 dins=[torch.empty((nb, n * m, n * m), dtype=torch.int64, device=dev)
                       for nb in sizes],
-                vals=[torch.empty(nb * max(T, 1) * m * m, dtype=torch.int64, device=dev)
-                      for nb in sizes],
+                vals=[torch.empty(nb * max(T, 1) * m * m if m <= 8 else 1, dtype=torch.int64,
+                                  device=dev) for nb in sizes],
                 base=[torch.empty(nb + 1, dtype=torch.int64, device=dev) for nb in sizes],
                 base_h=[torch.empty(nb + 1, dtype=torch.int64, pin_memory=True) for nb in sizes],
                 ws=[torch.empty(int(lib.fast_compact_workspace_bytes(nb)), dtype=torch.uint8,
@@ -394,17 +404,20 @@ class HostSynthPipeline:
                 _lib.check_rc(lib.fast_synth_batch_ev(ctypes.c_void_p(c["dins"][i].data_ptr()),
                                                       nb, n, m, ctypes.byref(bufs.struct), sh,
                                                       evs), "fast_synth_batch")
-                _lib.check_rc(lib.fast_compact_batch(ctypes.byref(bufs.struct), nb, n, m,
-                                                     ctypes.c_void_p(c["vals"][i].data_ptr()),
-                                                     ctypes.c_void_p(c["base"][i].data_ptr()),
-                                                     ctypes.c_void_p(c["ws"][i].data_ptr()), sh),
-                              "fast_compact_batch")
+                if m <= 8:
+                    _lib.check_rc(lib.fast_compact_batch(
+                        ctypes.byref(bufs.struct), nb, n, m,
+                        ctypes.c_void_p(c["vals"][i].data_ptr()),
+                        ctypes.c_void_p(c["base"][i].data_ptr()),
+                        ctypes.c_void_p(c["ws"][i].data_ptr()), sh), "fast_compact_batch")
+                else:  # no masks: no changed-cell values either
+                    c["base"][i].zero_()
                 if trace is not None:
                     trace.append(("synth", i, ev()))
                     trace[-1][2].record(st)
                 c["base_h"][i].copy_(c["base"][i], non_blocking=True)
                 c["events"][i].record(st)
-                for f in _COMPACT_FIELDS:
+                for f in out.fields:
                     getattr(out, f)[b0:b0 + nb].copy_(getattr(bufs, f), non_blocking=True)
                 if trace is not None:
                     trace.append(("d2h", i, ev()))

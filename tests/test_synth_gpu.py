@@ -239,7 +239,7 @@ def test_gpu_host_pipeline_stream_matches_oracle(depth):
             assert np.array_equal(p.moves[used], want["moves"][used]), (t, b)
 
 
-@pytest.mark.parametrize("n,m", [(16, 8), (8, 8), (5, 3), (3, 1)])
+@pytest.mark.parametrize("n,m", [(16, 8), (8, 8), (5, 3), (3, 1), (3, 16), (2, 12)])
 def test_gpu_compact_layout_matches_oracle(n, m):
     rng = np.random.default_rng(7 * n + m)
     B, G = 33, n * m
@@ -248,7 +248,8 @@ def test_gpu_compact_layout_matches_oracle(n, m):
     D[:, np.arange(G), np.arange(G)] = 0
     ref = oracle.synthesize_batch(D, n, m)
     hs = synth.synthesize_host_batch(torch.from_numpy(D).pin_memory(), n, m, chunk=10)
-    assert hs.nbytes() < synth.SynthBuffers(B, n, m, torch.device("cuda")).output_nbytes()
+    if m <= 8:  # m > 8 ships the balanced matrix itself (no 64-bit tile masks)
+        assert hs.nbytes() < synth.SynthBuffers(B, n, m, torch.device("cuda")).output_nbytes()
     for b in range(B):
         p = hs.packed(b, D[b])
         want = oracle.packed_fields(ref, b, n, m)
