@@ -590,6 +590,94 @@ __global__ void __launch_bounds__(kDecWarps * 32)
 }
 
 // ---------------------------------------------------------------------------
+// synth_small_kernel: the whole synthesis of one small matrix in ONE CTA
+// (n <= 6: stage capacity <= 32, so the decomposition warp also sorts) --
+// per-call latency for single small matrices (BASELINE configs 1-4) and the
+// alltoallv chain, where the balance / decompose launch pair (and the status
+// memset) cost more than their work.  Same per-tile code as balance_kernel
+// (validation, saturating server total, balance_senders, moves, mask), one
+// thread per tile straight from global memory, then decompose_one on warp 0.
+constexpr int kSmallThreads = 64;
+constexpr int kSmallMaxN = 6;
+
+__host__ __device__ inline size_t small_smem_bytes(int n, int m) {
+  return (((size_t)n * n * (m * m + 1) * 8 + 127) & ~(size_t)127) + dec_smem_bytes_t<1>(n);
+}
+
+template <int M, bool WB>
+__global__ void __launch_bounds__(kSmallThreads)
+    synth_small_kernel(const int64_t* __restrict__ D, const int n, const int m_rt,
+                       fast_sched_bufs out) {
+  extern __shared__ __align__(16) char ssm[];
+  pdl_trigger();
+  pdl_wait();  // D comes from the previous kernel of an alltoallv chain
+  const int m = M ? M : m_rt;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int G = n * m, TS = m * m + 1, T = n * (n - 1), slots = m > 1 ? m - 1 : 1;
+  const int64_t* Db = D + (int64_t)b * G * G;
+  int64_t* tiles = reinterpret_cast<int64_t*>(ssm);
+  int32_t* st = out.status + b;
+  if (tid == 0) *st = FAST_OK;
+  // coalesced stage-in of the whole matrix into tile-major shared memory
+  for (int x = tid; x < G * G; x += blockDim.x) {
+    const int r = x / G, c = x - r * G;
+    const int i = r / m, p = r - i * m, j = c / m, q = c - j * m;
+    tiles[(i * n + j) * TS + p * m + q] = __ldg(Db + x);
+  }
+  __syncthreads();
+  for (int t = tid; t < n * n; t += blockDim.x) {
+    const int i = t / n, j = t - i * n;
+    int64_t* tl = tiles + (int64_t)t * TS;
+    constexpr int MM = M ? M : 1;
+    int64_t rs[MM];
+    bool bad = false;
+    int64_t s = 0;
+#pragma unroll
+    for (int p = 0; p < MM; ++p) rs[p] = 0;
+    for (int p = 0; p < m; ++p) {
+      int64_t r = 0;
+      for (int q = 0; q < m; ++q) {
+        const int64_t v = tl[p * m + q];
+        r += v;
+        if (v < 0) { bad = true; continue; }
+        if (i == j && p == q && v != 0) bad = true;
+        s = sat_add(s, v);
+      }
+      if (M) {
+#pragma unroll
+        for (int pp = 0; pp < MM; ++pp)
+          if (pp == p) rs[pp] = r;
+      }
+    }
+    out.server[(int64_t)b * n * n + t] = s;
+    if (bad || s >= kMaxSafeTotal) {  // see balance_kernel
+      raise_status(st, FAST_EVALIDATION);
+    } else if (i != j) {
+      const int tidx = i * (n - 1) + (j < i ? j : j - 1);
+      uint64_t mk = 0;
+      int nm = balance_tile<M>(tl, m, out.moves + ((int64_t)b * T + tidx) * slots, slots,
+                               M ? rs : nullptr, &mk);
+      if (out.tile_mask) out.tile_mask[(int64_t)b * T + tidx] = mk;
+      if (nm < 0) {
+        raise_status(st, FAST_EINVARIANT);
+        nm = 0;
+      }
+      out.move_count[(int64_t)b * T + tidx] = nm;
+    }
+  }
+  __syncthreads();  // balanced tiles, server totals and status are in place
+  int64_t* Bb = out.balanced + (int64_t)b * G * G;
+  for (int x = tid; x < G * G; x += blockDim.x) {
+    const int r = x / G, c = x - r * G;
+    const int i = r / m, p = r - i * m, j = c / m, q = c - j * m;
+    Bb[x] = tiles[(i * n + j) * TS + p * m + q];
+  }
+  if (tid < 32)
+    decompose_one<1, WB>(ssm + (small_smem_bytes(n, m) - dec_smem_bytes_t<1>(n)), out.server,
+                         b, n, FAST_DEC_SERVER, 1, out, tid);
+}
+
+// ---------------------------------------------------------------------------
 // sort_stages_ascending (birkhoff.py:255-266): sort of the kept stages by
 // (weight, src0, dst0, raw index) -- the raw index makes it equal to
 // Python's stable sort.  Bitonic network in the "flip" form (every merge
@@ -1044,6 +1132,36 @@ int launch_decompose(const int64_t* S, int B, int n, int mode, int check_total,
   return check(launch_k(sort_kernel, dim3(B), dim3(threads), ssmem, s, pdl, n, *out));
 }
 
+// One-launch synthesis for small n (synth_small_kernel).  Returns -1 (not
+// an error code: the caller takes the batched kernels) when the shape does
+// not fit; the even-m alignment contract is the same as launch_balance's.
+int launch_synth_small(const int64_t* D, int B, int n, int m, const fast_sched_bufs* out,
+                       cudaStream_t s, bool pdl) {
+  const size_t smem = small_smem_bytes(n, m);
+#ifdef FAST_NO_SMALL  // A/B: always the batched kernels
+  return -1;
+#endif
+  if (n > kSmallMaxN || smem > 48 * 1024) return -1;
+  if (m % 2 == 0 && (((uintptr_t)D | (uintptr_t)out->balanced) & 15)) return FAST_EVALIDATION;
+  const bool wb = out->stage_bytes != nullptr;
+  cudaError_t e;
+#define FAST_SMALL(MV)                                                                  \
+  e = wb ? launch_k(synth_small_kernel<MV, true>, dim3(B), dim3(kSmallThreads), smem, s, \
+                    pdl, D, n, m, *out)                                                 \
+         : launch_k(synth_small_kernel<MV, false>, dim3(B), dim3(kSmallThreads), smem, s, \
+                    pdl, D, n, m, *out)
+  switch (m) {
+    case 1: FAST_SMALL(1); break;
+    case 2: FAST_SMALL(2); break;
+    case 4: FAST_SMALL(4); break;
+    case 8: FAST_SMALL(8); break;
+    default: FAST_SMALL(0);
+  }
+#undef FAST_SMALL
+  if (e != cudaSuccess) return FAST_ECUDA;
+  return check(cudaGetLastError());
+}
+
 bool bad_shape(int B, int n, int m) {
   return B < 0 || n < 2 || n > FAST_MAX_SERVERS || m < 1 ||
          m > FAST_MAX_GPUS_PER_SERVER;
@@ -1122,6 +1240,14 @@ int fast_synth_batch_ev(const int64_t* D, int B, int n, int m,
   cudaStream_t s = (cudaStream_t)stream;
   cudaEvent_t const* ev = (cudaEvent_t const*)events;
   if (ev && cudaEventRecord(ev[0], s) != cudaSuccess) return FAST_ECUDA;
+  if (!ev) {  // per-kernel events need the separate kernels
+    const int rs = launch_synth_small(D, B, n, m, out, s, false);
+    if (rs != -1) {
+      if (rs != FAST_OK || !out->strip) return rs;
+      strip_table_kernel<<<B, kStripThreads, 0, s>>>(n, *out);
+      return cudaGetLastError() == cudaSuccess ? FAST_OK : FAST_ECUDA;
+    }
+  }
   if (cudaMemsetAsync(out->status, 0, sizeof(int32_t) * B, s) != cudaSuccess)
     return FAST_ECUDA;
   int rc = launch_balance(D, B, n, m, out, s);
@@ -1149,6 +1275,8 @@ int fast_synth_batch_chain(const int64_t* D, int B, int n, int m, const fast_sch
                            cudaStream_t s, bool pdl) {
   if (bad_shape(B, n, m) || !out) return FAST_EVALIDATION;
   if (B == 0) return FAST_OK;
+  const int rs = launch_synth_small(D, B, n, m, out, s, pdl);
+  if (rs != -1) return rs;
   int rc = launch_balance(D, B, n, m, out, s, pdl);
   if (rc != FAST_OK) return rc;
   return launch_decompose(out->server, B, n, FAST_DEC_SERVER, 1, out, s, nullptr, pdl);
