@@ -5,7 +5,7 @@ import torch
 from paper_2505_09764_b200 import _lib, synth, workloads
 lib = _lib.load()
 tag = os.path.basename(os.environ.get("FASTB200_LIB", "product"))
-for (n, m, B) in [(4, 8, 1000), (6, 8, 1000), (2, 4, 4096)]:
+for (n, m, B) in [(4, 8, 1000), (6, 8, 1000), (2, 4, 4096), (8, 8, 1000), (12, 8, 1000)]:
     D = workloads.zipf_batch_device(range(B), n*m, 1.2, 1 << 28, "cuda")
     bufs = synth.SynthBuffers(B, n, m)
     s = torch.cuda.current_stream()

@@ -13,7 +13,7 @@ from paper_2505_09764_b200 import _lib, synth, workloads  # noqa: E402
 lib = _lib.load()
 tag = os.path.basename(os.environ.get("FASTB200_LIB", "product"))
 res = []
-for n, m in [(2, 1), (2, 2), (4, 1), (2, 4), (4, 2), (4, 8), (6, 8), (8, 8)]:
+for n, m in [(2, 1), (2, 2), (4, 1), (2, 4), (4, 2), (4, 8), (6, 8), (8, 8), (10, 8), (12, 8), (12, 4), (16, 8)]:
     D = torch.from_numpy(workloads.zipf_sizes(0, n * m, 1.2, 1 << 28)).cuda().view(1, n * m, n * m)
     bufs = synth.SynthBuffers(1, n, m)
     s = torch.cuda.Stream()
