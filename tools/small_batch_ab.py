@@ -1,8 +1,13 @@
-import ctypes, os, sys
-sys.path.insert(0, '/root/repo') if os.path.exists('/root/repo') else None
-sys.path.insert(0, os.getcwd())
-import torch
-from paper_2505_09764_b200 import _lib, synth, workloads
+"""Synthesis time of batches of small matrices for the library in
+FASTB200_LIB (A/B of the one-launch small-n kernel).
+    python tools/small_batch_ab.py"""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+from paper_2505_09764_b200 import _lib, synth, workloads  # noqa: E402
 lib = _lib.load()
 tag = os.path.basename(os.environ.get("FASTB200_LIB", "product"))
 for (n, m, B) in [(4, 8, 1000), (6, 8, 1000), (2, 4, 4096), (8, 8, 1000), (12, 8, 1000)]:
