@@ -278,7 +278,13 @@ __device__ __forceinline__ void bal_tile_work(int64_t* __restrict__ t,
     int nm = 0;
     (void)mv;
 #else
+#ifndef FAST_BAL_NO32
+    // tile total below 2^31 (no negative cells here): the greedy in 32 bits
+    int nm = tp < ((int64_t)1 << 31) ? balance_tile<M, int32_t>(t, M, mv, slots, rs, &mk)
+                                     : balance_tile<M>(t, M, mv, slots, rs, &mk);
+#else
     int nm = balance_tile<M>(t, M, mv, slots, rs, &mk);
+#endif
 #endif
     if (out.tile_mask) out.tile_mask[(int64_t)b * T + tidx] = mk;
     if (nm < 0) {

@@ -33,30 +33,33 @@ __host__ __device__ __forceinline__ int stage_cap(int n) {
 
 // ---------------------------------------------------------------------------
 // balance_senders (balance.py:77-126) on one m x m tile in shared memory.
-// Returns the number of moves, or -1 if an invariant breaks.
-template <int M>
+// Returns the number of moves, or -1 if an invariant breaks.  V is the
+// arithmetic type of the greedy: int64_t in general, int32_t when the caller
+// knows the tile total (hence every cell, row sum, deviation and chunk) is
+// below 2^31 -- the same exact integer steps at half the ALU cost.
+template <int M, typename V = int64_t>
 __device__ __forceinline__ int balance_tile(int64_t* __restrict__ t, const int m_rt,
                             fast_move* __restrict__ out, const int slots,
                             const int64_t* rowsum = nullptr,
                             uint64_t* changed = nullptr) {
   constexpr int MM = M ? M : FAST_MAX_GPUS_PER_SERVER;
   const int m = M ? M : m_rt;
-  int64_t dev[MM];
-  int64_t total = 0;
+  V dev[MM];
+  V total = 0;
 #pragma unroll
   for (int p = 0; p < MM; ++p) {
-    int64_t s = 0;
+    V s = 0;
     if (p < m) {
       if (rowsum) {
-        s = rowsum[p];  // caller already summed the rows
+        s = (V)rowsum[p];  // caller already summed the rows
       } else {
-        for (int q = 0; q < m; ++q) s += t[p * m + q];
+        for (int q = 0; q < m; ++q) s += (V)t[p * m + q];
       }
     }
     dev[p] = s;
     total += s;
   }
-  const int64_t base = total / m, extra = total % m;
+  const V base = total / m, extra = total % m;
 #pragma unroll
   for (int p = 0; p < MM; ++p)
     if (p < m) dev[p] -= base + (p < extra ? 1 : 0);
@@ -69,11 +72,11 @@ __device__ __forceinline__ int balance_tile(int64_t* __restrict__ t, const int m
     // over[0]: largest positive deviation, lowest index on ties;
     // under[0]: most negative deviation, lowest index on ties.
     int g = -1, h = -1;
-    int64_t dg = 0, dh = 0;
+    V dg = 0, dh = 0;
 #pragma unroll
     for (int p = 0; p < MM; ++p) {
       if (p < m) {
-        const int64_t d = dev[p];
+        const V d = dev[p];
         if (d > dg) { dg = d; g = p; }
         if (d < dh) { dh = d; h = p; }
       }
@@ -83,19 +86,19 @@ __device__ __forceinline__ int balance_tile(int64_t* __restrict__ t, const int m
       return nmoves;
     }
     if (h < 0 || nmoves >= slots) return -1;
-    const int64_t chunk = dg < -dh ? dg : -dh;
-    int64_t left = chunk;
+    const V chunk = dg < -dh ? dg : -dh;
+    V left = chunk;
     int guard = 0;
     int64_t* rg = t + g * m;
     int64_t* rh = t + h * m;
     while (left > 0) {
       int q = 0;  // np.argmax: first maximum of row g
-      int64_t best = rg[0];
+      V best = (V)rg[0];
       for (int c = 1; c < m; ++c) {
-        const int64_t x = rg[c];
+        const V x = (V)rg[c];
         if (x > best) { best = x; q = c; }
       }
-      const int64_t take = left < best ? left : best;
+      const V take = left < best ? left : best;
       if (take <= 0 || ++guard > m) return -1;
       rg[q] -= take;
       rh[q] += take;
